@@ -1,0 +1,247 @@
+"""CPU oracle for the ActNN hot path ("ACTNN-Q v1"), ctypes binding.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_2104_14129_b200`` never imports it and
+shares no code with it ("Oracle").
+
+Every function is a thin numpy marshalling layer over ``actnn_oracle.cpp``;
+the arithmetic lives there, each step citing the PAPER.md passage it follows.
+Functions without an external pin would say "parity unpinned" here; none do
+(the pins are listed in DESIGN.md, "Oracle pins").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+_lock = threading.Lock()
+
+F32, BF16 = 0, 1
+LEVELS_POW2 = (1 << 1) | (1 << 2) | (1 << 4) | (1 << 8)   # {1,2,4,8}, the hot path
+LEVELS_UNIT = 0x1FE                                      # 1..8, the paper's unit step
+ERR_BUDGET = -3
+
+
+def build() -> str:
+    """Compile liboracle.so with the oracle's own Makefile (-ffp-contract=off)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        src = os.path.join(_HERE, "actnn_oracle.cpp")
+        if (not os.path.exists(_LIB_PATH)
+                or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src)):
+            build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        P, I64, I32, U64, U32 = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                 ctypes.c_uint64, ctypes.c_uint32)
+        sig = {
+            "oracle_philox4x32_10": (None, [P, P, P]),
+            "oracle_random14": (U32, [U64, U64]),
+            "oracle_group_minmax": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I32, P, P]),
+            "oracle_sensitivity": (None, [P, P, I64, I64, P]),
+            "oracle_allocate_bits": (ctypes.c_int, [P, I64, I64, U32, P]),
+            "oracle_objective": (ctypes.c_double, [P, P, I64]),
+            "oracle_allocate_bruteforce": (ctypes.c_double, [P, I64, I64, U32, P]),
+            "oracle_allocate_dp": (ctypes.c_double, [P, I64, I64, U32, P]),
+            "oracle_offsets": (None, [P, I64, I64, I32, P]),
+            "oracle_quantize_group": (ctypes.c_int, [P, I32, I32, I32, U64, U64, P, P, P]),
+            "oracle_quantize": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I32, P, U64, I64,
+                                               P, P, P, ctypes.c_int]),
+            "oracle_dequantize": (ctypes.c_int, [P, P, P, P, I64, I64, I32, P, ctypes.c_int,
+                                                 ctypes.c_int]),
+            "oracle_dequantize_group": (None, [P, I32, I32, ctypes.c_float, ctypes.c_float,
+                                               P, P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"], "oracle arrays must be C-contiguous"
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _as_x(x: np.ndarray):
+    """fp32 arrays pass as F32; bf16 tensors pass as their uint16 bit patterns."""
+    x = np.ascontiguousarray(x)
+    if x.dtype == np.float32:
+        return x, F32
+    if x.dtype == np.uint16:
+        return x, BF16
+    raise TypeError(f"oracle input must be float32 or uint16 (bf16 bits), got {x.dtype}")
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    o = np.zeros(4, dtype=np.uint32)
+    _load().oracle_philox4x32_10(_ptr(c), _ptr(k), _ptr(o))
+    return o
+
+
+def random14(seed: int, e: int) -> int:
+    return int(_load().oracle_random14(seed, e))
+
+
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def group_minmax(x: np.ndarray, G: int = 256):
+    """x: [N, D] fp32 or bf16 bits -> (gmin, gmax) each [N, ceil(D/G)] fp32."""
+    x, dt = _as_x(x)
+    N, D = x.shape
+    ng = ceil_div(D, G)
+    gmin = np.zeros((N, ng), np.float32)
+    gmax = np.zeros((N, ng), np.float32)
+    st = _load().oracle_group_minmax(_ptr(x), dt, N, D, G, _ptr(gmin), _ptr(gmax))
+    assert st == 0, st
+    return gmin, gmax
+
+
+def sensitivity(gmin: np.ndarray, gmax: np.ndarray) -> np.ndarray:
+    """S_n = ||R_n||^2 in the canonical order (fp64 [N])."""
+    gmin = np.ascontiguousarray(gmin, np.float32)
+    gmax = np.ascontiguousarray(gmax, np.float32)
+    N, ng = gmin.shape
+    S = np.zeros(N, np.float64)
+    _load().oracle_sensitivity(_ptr(gmin), _ptr(gmax), N, ng, _ptr(S))
+    return S
+
+
+def allocate_bits(w: np.ndarray, budget: int, level_mask: int = LEVELS_POW2) -> np.ndarray:
+    """Heap greedy.  Raises ValueError when the budget is infeasible."""
+    w = np.ascontiguousarray(w, np.float64)
+    bits = np.zeros(len(w), np.uint8)
+    st = _load().oracle_allocate_bits(_ptr(w), len(w), int(budget), level_mask, _ptr(bits))
+    if st != 0:
+        raise ValueError(f"oracle_allocate_bits failed: {st}")
+    return bits
+
+
+def objective(w: np.ndarray, bits: np.ndarray) -> float:
+    w = np.ascontiguousarray(w, np.float64)
+    bits = np.ascontiguousarray(bits, np.uint8)
+    return float(_load().oracle_objective(_ptr(w), _ptr(bits), len(w)))
+
+
+def allocate_bruteforce(w, budget, level_mask=LEVELS_POW2):
+    w = np.ascontiguousarray(w, np.float64)
+    bits = np.zeros(len(w), np.uint8)
+    obj = _load().oracle_allocate_bruteforce(_ptr(w), len(w), int(budget), level_mask,
+                                             _ptr(bits))
+    return obj, bits
+
+
+def allocate_dp(w, budget, level_mask=LEVELS_POW2):
+    w = np.ascontiguousarray(w, np.float64)
+    bits = np.zeros(len(w), np.uint8)
+    obj = _load().oracle_allocate_dp(_ptr(w), len(w), int(budget), level_mask, _ptr(bits))
+    return obj, bits
+
+
+def offsets(bits: np.ndarray, D: int, G: int = 256) -> np.ndarray:
+    bits = np.ascontiguousarray(bits, np.uint8)
+    off = np.zeros(len(bits) + 1, np.int64)
+    _load().oracle_offsets(_ptr(bits), len(bits), D, G, _ptr(off))
+    return off
+
+
+def quantize_group(h: np.ndarray, b: int, seed: int, e0: int, G: int = 256):
+    """One group (len(h) <= G) whose first element has global index e0.
+    Returns (segment bytes [G*b/8], zmin, scale)."""
+    h = np.ascontiguousarray(h, np.float32)
+    seg = np.zeros(G * b // 8, np.uint8)
+    z = ctypes.c_float()
+    s = ctypes.c_float()
+    st = _load().oracle_quantize_group(_ptr(h), len(h), G, b, seed, e0, _ptr(seg),
+                                       ctypes.byref(z), ctypes.byref(s))
+    if st != 0:
+        raise ValueError(f"oracle_quantize_group failed: {st}")
+    return seg, np.float32(z.value), np.float32(s.value)
+
+
+def quantize(x: np.ndarray, bits, seed: int, sample_base: int = 0, G: int = 256,
+             threads: int = 1):
+    """x [N, D] -> (packed u8 [off[N]], zmin [N, ng], scale [N, ng], off [N+1])."""
+    x, dt = _as_x(x)
+    N, D = x.shape
+    bits = np.ascontiguousarray(np.broadcast_to(np.asarray(bits, np.uint8), (N,)))
+    off = offsets(bits, D, G)
+    ng = ceil_div(D, G)
+    packed = np.zeros(int(off[-1]), np.uint8)
+    zmin = np.zeros((N, ng), np.float32)
+    scale = np.zeros((N, ng), np.float32)
+    st = _load().oracle_quantize(_ptr(x), dt, N, D, G, _ptr(bits), seed, sample_base,
+                                 _ptr(packed), _ptr(zmin), _ptr(scale), threads)
+    if st != 0:
+        raise ValueError(f"oracle_quantize failed: {st}")
+    return packed, zmin, scale, off
+
+
+def dequantize(packed, zmin, scale, bits, N: int, D: int, G: int = 256,
+               out_dtype: int = F32, threads: int = 1) -> np.ndarray:
+    """-> [N, D] fp32, or uint16 bf16 bit patterns when out_dtype == BF16."""
+    bits = np.ascontiguousarray(np.broadcast_to(np.asarray(bits, np.uint8), (N,)))
+    packed = np.ascontiguousarray(packed, np.uint8)
+    zmin = np.ascontiguousarray(zmin, np.float32)
+    scale = np.ascontiguousarray(scale, np.float32)
+    out = np.zeros((N, D), np.float32 if out_dtype == F32 else np.uint16)
+    st = _load().oracle_dequantize(_ptr(packed), _ptr(zmin), _ptr(scale), _ptr(bits), N, D, G,
+                                   _ptr(out), out_dtype, threads)
+    if st != 0:
+        raise ValueError(f"oracle_dequantize failed: {st}")
+    return out
+
+
+def dequantize_group(seg, length: int, b: int, zmin: float, scale: float):
+    seg = np.ascontiguousarray(seg, np.uint8)
+    codes = np.zeros(length, np.uint32)
+    out = np.zeros(length, np.float32)
+    _load().oracle_dequantize_group(_ptr(seg), length, b, float(zmin), float(scale),
+                                    _ptr(codes), _ptr(out))
+    return codes, out
+
+
+def sharded_quantize(x: np.ndarray, k: int, avg_bits: float, seed: int,
+                     level_mask: int = LEVELS_POW2, G: int = 256, threads: int = 1):
+    """O13: k virtual ranks.  Rank r owns samples [r*N/k, (r+1)*N/k); it writes
+    its S_n into a zero array of length N, the k arrays are summed (the
+    all-reduce), every rank allocates over all N samples with budget
+    floor(avg_bits * N), then quantizes its slice with sample_base = r*N/k.
+    Returns the per-rank (packed, zmin, scale, bits) tuples."""
+    x, _ = _as_x(x)
+    N, D = x.shape
+    assert N % k == 0
+    n_loc = N // k
+    total = np.zeros(N, np.float64)
+    for r in range(k):
+        gmin, gmax = group_minmax(x[r * n_loc:(r + 1) * n_loc], G)
+        part = np.zeros(N, np.float64)
+        part[r * n_loc:(r + 1) * n_loc] = sensitivity(gmin, gmax)
+        total = total + part
+    bits = allocate_bits(total, int(np.floor(avg_bits * N)), level_mask)
+    out = []
+    for r in range(k):
+        sl = slice(r * n_loc, (r + 1) * n_loc)
+        packed, zmin, scale, _ = quantize(x[sl], bits[sl], seed, r * n_loc, G, threads)
+        out.append((packed, zmin, scale, bits[sl]))
+    return out

@@ -1,0 +1,417 @@
+/*
+ * actnn_oracle.cpp -- the CPU oracle ("ACTNN-Q v1"), plain and slow on purpose.
+ *
+ * TEST INFRASTRUCTURE ONLY (see actnn_oracle.h).  Every function follows the
+ * passage it cites step by step; there is no blocking, vectorisation or fusion.
+ * The CUDA path (paper_2104_14129_b200/csrc) is an independent implementation.
+ *
+ * Build: g++ -std=c++17 -O2 -ffp-contract=off -fno-fast-math -fPIC -shared
+ */
+#include "actnn_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <queue>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+/* ------------------------------------------------------------------------- */
+/* Philox4x32-10.  Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as    */
+/* easy as 1, 2, 3" (SC'11): round multipliers 0xD2511F53 / 0xCD9E8D57, Weyl   */
+/* key bumps 0x9E3779B9 / 0xBB67AE85, 10 rounds, the key bumped between rounds.*/
+/* DESIGN reading 7: the paper needs "stochastic rounding" but     */
+/* names no generator; SPEC asks for a counter-based one.               */
+/* ------------------------------------------------------------------------- */
+extern "C" void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2],
+                                     uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* O6: element e draws 16-bit lane (e & 7) of Philox(ctr = e >> 3, key = seed)
+ * and keeps its low 14 bits.  (DESIGN reading 6: 14-bit fixed-point SR.) */
+extern "C" uint32_t oracle_random14(uint64_t seed, uint64_t e) {
+    uint64_t block = e >> 3;
+    uint32_t ctr[4] = {(uint32_t)block, (uint32_t)(block >> 32), 0u, 0u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t o[4];
+    oracle_philox4x32_10(ctr, key, o);
+    uint32_t j = (uint32_t)(e & 7u);
+    uint32_t word = o[j >> 1];
+    uint32_t half = (j & 1u) ? (word >> 16) : (word & 0xFFFFu);
+    return half & 0x3FFFu;
+}
+
+/* O1: widen one element to fp32 (bf16 -> fp32 is exact: bits << 16). */
+static float widen(const void* x, int dtype, int64_t idx) {
+    if (dtype == ORACLE_F32) return ((const float*)x)[idx];
+    uint16_t h = ((const uint16_t*)x)[idx];
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+/* RNE of an fp32 value to bf16 (DESIGN reading 15), finite inputs. */
+static uint16_t to_bf16_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu)) return 0x7FC0u; /* NaN */
+    uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7FFFu + lsb;
+    return (uint16_t)(u >> 16);
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+/* O3 for one group: exact min and max, each canonicalised (x + 0.0f maps -0
+ * to +0; DESIGN reading 17).  P:493-498: Z = min h, R = max h - min h. */
+static void group_min_max(const float* h, int32_t len, float* Z, float* M) {
+    float z = h[0], m = h[0];
+    for (int32_t k = 1; k < len; ++k) {
+        if (h[k] < z) z = h[k];
+        if (h[k] > m) m = h[k];
+    }
+    *Z = z + 0.0f;
+    *M = m + 0.0f;
+}
+
+extern "C" int oracle_group_minmax(const void* x, int dtype, int64_t N, int64_t D, int32_t G,
+                                   float* gmin, float* gmax) {
+    if (N < 0 || D < 0 || G < 1) return ORACLE_ERR_INVALID;
+    int64_t ng = ceil_div(D, G);
+    std::vector<float> h(G);
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t i = 0; i < ng; ++i) {
+            int32_t len = (int32_t)std::min<int64_t>(G, D - i * G);
+            for (int32_t k = 0; k < len; ++k) h[k] = widen(x, dtype, n * D + i * G + k);
+            group_min_max(h.data(), len, &gmin[n * ng + i], &gmax[n * ng + i]);
+        }
+    }
+    return ORACLE_OK;
+}
+
+/* O11: S_n = sum_i R_ni^2 (the ||R_n||^2 factor of w_n, P:547 / Eq. 7).
+ * Canonical order (DESIGN reading 11): chunks of 32 consecutive groups
+ * (zero padded), v[l] = R_l^2 exactly in fp64, then for o = 16,8,4,2,1 every
+ * v[l] <- v[l] + v[l^o] simultaneously; T_c = v[0]; S_n = ((0+T_0)+T_1)+... */
+extern "C" void oracle_sensitivity(const float* gmin, const float* gmax, int64_t N,
+                                   int64_t ng, double* S) {
+    int64_t nch = ceil_div(ng, 32);
+    for (int64_t n = 0; n < N; ++n) {
+        double s = 0.0;
+        for (int64_t c = 0; c < nch; ++c) {
+            double v[32], t[32];
+            for (int l = 0; l < 32; ++l) {
+                int64_t i = c * 32 + l;
+                if (i < ng) {
+                    float R = gmax[n * ng + i] - gmin[n * ng + i];
+                    v[l] = (double)R * (double)R;
+                } else {
+                    v[l] = 0.0;
+                }
+            }
+            for (int o = 16; o >= 1; o >>= 1) {
+                for (int l = 0; l < 32; ++l) t[l] = v[l] + v[l ^ o];
+                for (int l = 0; l < 32; ++l) v[l] = t[l];
+            }
+            s = s + v[0];
+        }
+        S[n] = s;
+    }
+}
+
+/* Levels of the mask in descending order (the greedy starts at the top). */
+static int mask_levels(uint32_t level_mask, int* L) {
+    if (level_mask == 0 || (level_mask & ~0x1FEu)) return -1;
+    int m = 0;
+    for (int b = 8; b >= 1; --b)
+        if (level_mask & (1u << b)) L[m++] = b;
+    return m;
+}
+
+/* 1 / B^2 with B = 2^b - 1 (Eq. 8). */
+static double inv_B2(int b) {
+    double B = (double)((1 << b) - 1);
+    return 1.0 / (B * B);
+}
+
+/* O12: the paper's greedy: "starts with high numerical precision ...
+ * progressively reduces the precision until it fits in the total bits budget.
+ * In each move, it chooses a b to reduce ..., such that the increment of
+ * variance is minimal.  With a binary heap for picking up the optimal move".
+ * Move (n, c) takes sample n from level L[c] to L[c+1]; its priority is the
+ * variance increase per freed bit, w_n (1/B_{c+1}^2 - 1/B_c^2) / (L[c]-L[c+1])
+ * (DESIGN reading 9); ties break by sample index, then move index. */
+extern "C" int oracle_allocate_bits(const double* w, int64_t N, int64_t budget,
+                                    uint32_t level_mask, uint8_t* bits) {
+    int L[8];
+    int m = mask_levels(level_mask, L);
+    if (m < 1 || N < 0) return ORACLE_ERR_INVALID;
+    if (budget < N * (int64_t)L[m - 1]) return ORACLE_ERR_BUDGET;
+    double slope[8];
+    for (int c = 0; c + 1 < m; ++c)
+        slope[c] = (inv_B2(L[c + 1]) - inv_B2(L[c])) / (double)(L[c] - L[c + 1]);
+
+    std::vector<int> lvl((size_t)N, 0);
+    int64_t total = N * (int64_t)L[0];
+    typedef std::tuple<double, int64_t, int> Move; /* (key, n, c) */
+    std::priority_queue<Move, std::vector<Move>, std::greater<Move>> heap;
+    if (m > 1)
+        for (int64_t n = 0; n < N; ++n) heap.push(Move(w[n] * slope[0], n, 0));
+    while (total > budget) {
+        Move mv = heap.top();
+        heap.pop();
+        int64_t n = std::get<1>(mv);
+        int c = std::get<2>(mv);
+        lvl[n] = c + 1;
+        total -= (int64_t)(L[c] - L[c + 1]);
+        if (c + 2 < m) heap.push(Move(w[n] * slope[c + 1], n, c + 1));
+    }
+    for (int64_t n = 0; n < N; ++n) bits[n] = (uint8_t)L[lvl[n]];
+    return ORACLE_OK;
+}
+
+extern "C" double oracle_objective(const double* w, const uint8_t* bits, int64_t N) {
+    double s = 0.0;
+    for (int64_t n = 0; n < N; ++n) {
+        double B = (double)((1 << bits[n]) - 1);
+        s += w[n] / (B * B);
+    }
+    return s;
+}
+
+/* Exhaustive search over all level assignments (tiny N only). */
+static void brute_rec(const double* w, int64_t N, int64_t budget, const int* L, int m,
+                      int64_t n, int64_t used, std::vector<uint8_t>& cur,
+                      std::vector<uint8_t>& best, double& best_obj) {
+    if (n == N) {
+        double obj = oracle_objective(w, cur.data(), N);
+        if (obj < best_obj) {
+            best_obj = obj;
+            best = cur;
+        }
+        return;
+    }
+    for (int c = 0; c < m; ++c) {
+        if (used + L[c] + (N - n - 1) * (int64_t)L[m - 1] > budget) continue;
+        cur[n] = (uint8_t)L[c];
+        brute_rec(w, N, budget, L, m, n + 1, used + L[c], cur, best, best_obj);
+    }
+}
+
+extern "C" double oracle_allocate_bruteforce(const double* w, int64_t N, int64_t budget,
+                                             uint32_t level_mask, uint8_t* bits) {
+    int L[8];
+    int m = mask_levels(level_mask, L);
+    if (m < 1 || N < 0 || N > 12 || budget < N * (int64_t)L[m - 1]) return -1.0;
+    std::vector<uint8_t> cur((size_t)N), best((size_t)N);
+    double best_obj = HUGE_VAL;
+    brute_rec(w, N, budget, L, m, 0, 0, cur, best, best_obj);
+    for (int64_t n = 0; n < N; ++n) bits[n] = best[n];
+    return oracle_objective(w, bits, N);
+}
+
+/* Knapsack DP over (sample, bits used): "can be solved exactly by DP". */
+extern "C" double oracle_allocate_dp(const double* w, int64_t N, int64_t budget,
+                                     uint32_t level_mask, uint8_t* bits) {
+    int L[8];
+    int m = mask_levels(level_mask, L);
+    if (m < 1 || N < 0 || budget < N * (int64_t)L[m - 1]) return -1.0;
+    int64_t cap = std::min<int64_t>(budget, N * (int64_t)L[0]);
+    const double INF = HUGE_VAL;
+    /* dp[n][u]: min objective of samples < n using exactly u bits */
+    std::vector<std::vector<double>> dp((size_t)N + 1, std::vector<double>((size_t)cap + 1, INF));
+    std::vector<std::vector<int8_t>> choice((size_t)N + 1,
+                                            std::vector<int8_t>((size_t)cap + 1, -1));
+    dp[0][0] = 0.0;
+    for (int64_t n = 0; n < N; ++n)
+        for (int64_t u = 0; u <= cap; ++u) {
+            if (dp[n][u] == INF) continue;
+            for (int c = 0; c < m; ++c) {
+                int64_t v = u + L[c];
+                if (v > cap) continue;
+                double B = (double)((1 << L[c]) - 1);
+                double o = dp[n][u] + w[n] / (B * B);
+                if (o < dp[n + 1][v]) {
+                    dp[n + 1][v] = o;
+                    choice[n + 1][v] = (int8_t)c;
+                }
+            }
+        }
+    int64_t bu = -1;
+    for (int64_t u = 0; u <= cap; ++u)
+        if (dp[N][u] < INF && (bu < 0 || dp[N][u] < dp[N][bu])) bu = u;
+    if (bu < 0) return -1.0;
+    int64_t u = bu;
+    for (int64_t n = N; n >= 1; --n) {
+        int c = choice[n][u];
+        bits[n - 1] = (uint8_t)L[c];
+        u -= L[c];
+    }
+    return oracle_objective(w, bits, N);
+}
+
+/* O8: sample n's segment holds b_n * ceil(D/G) * G / 8 bytes. */
+extern "C" void oracle_offsets(const uint8_t* bits, int64_t N, int64_t D, int32_t G,
+                               int64_t* off) {
+    int64_t ng = ceil_div(D, G);
+    off[0] = 0;
+    for (int64_t n = 0; n < N; ++n) off[n + 1] = off[n] + (int64_t)bits[n] * ng * G / 8;
+}
+
+/* O3-O9 for one group, in the paper's order:
+ *   Z = min, R = max - min                           (O3)
+ *   u_bar = B (h - Z) / R as the 14-bit fixed point  (O4-O5)
+ *       q = RNE(RN(h - Z) * RN(B / R) * 2^14)
+ *   u_hat = ceil(u_bar) w.p. frac(u_bar) else floor   (O6-O7)
+ *       code = (q + r) >> 14 with r uniform in [0, 2^14)
+ *   codes LSB-first into a bit stream                (O8)
+ */
+extern "C" int oracle_quantize_group(const float* h, int32_t len, int32_t G, int32_t b,
+                                     uint64_t seed, uint64_t e0, uint8_t* seg, float* zmin,
+                                     float* scale) {
+    float Z, M;
+    group_min_max(h, len, &Z, &M);
+    float R = M - Z;
+    uint32_t B = (1u << b) - 1u;
+    float Bf = (float)B;
+    *zmin = Z;
+    *scale = R / Bf;
+    /* degenerate group (DESIGN reading 16): every code 0, dequantises to Z */
+    float inv14 = (R < 0x1p-96f) ? 0.0f : (Bf / R) * 16384.0f;
+    std::memset(seg, 0, (size_t)G * (size_t)b / 8);
+    for (int32_t k = 0; k < len; ++k) {
+        float delta = h[k] - Z;
+        /* 24b x 24b product is exact in binary64; nearbyint is RNE */
+        double qd = std::nearbyint((double)delta * (double)inv14);
+        uint64_t q = (uint64_t)qd;
+        if (q > ((uint64_t)B << 14)) return ORACLE_ERR_INVARIANT;
+        uint64_t r = oracle_random14(seed, e0 + (uint64_t)k);
+        uint32_t code = (uint32_t)((q + r) >> 14);
+        for (int32_t t = 0; t < b; ++t) {
+            int64_t bit = (int64_t)k * b + t;
+            if ((code >> t) & 1u) seg[bit >> 3] |= (uint8_t)(1u << (bit & 7));
+        }
+    }
+    return ORACLE_OK;
+}
+
+/* Samples [n0, n1) of a tensor; shared by the thread fan-out below. */
+static int quantize_range(const void* x, int dtype, int64_t n0, int64_t n1, int64_t D,
+                          int32_t G, const uint8_t* bits, const int64_t* off, uint64_t seed,
+                          int64_t sample_base, uint8_t* packed, float* zmin, float* scale) {
+    int64_t ng = ceil_div(D, G);
+    std::vector<float> h(G);
+    for (int64_t n = n0; n < n1; ++n) {
+        int32_t b = bits[n];
+        for (int64_t i = 0; i < ng; ++i) {
+            int32_t len = (int32_t)std::min<int64_t>(G, D - i * G);
+            for (int32_t k = 0; k < len; ++k) h[k] = widen(x, dtype, n * D + i * G + k);
+            uint64_t e0 = (uint64_t)(sample_base + n) * (uint64_t)D + (uint64_t)(i * G);
+            uint8_t* seg = packed + off[n] + i * (int64_t)G * b / 8;
+            int st = oracle_quantize_group(h.data(), len, G, b, seed, e0, seg,
+                                           &zmin[n * ng + i], &scale[n * ng + i]);
+            if (st != ORACLE_OK) return st;
+        }
+    }
+    return ORACLE_OK;
+}
+
+static bool bits_ok(const uint8_t* bits, int64_t N) {
+    for (int64_t n = 0; n < N; ++n)
+        if (bits[n] < 1 || bits[n] > 8) return false;
+    return true;
+}
+
+template <class F>
+static int fan_out(int64_t N, int threads, F fn) {
+    if (threads < 1) threads = 1;
+    if (threads > N) threads = (int)(N > 0 ? N : 1);
+    std::vector<int> st((size_t)threads, ORACLE_OK);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+        int64_t n0 = N * t / threads, n1 = N * (t + 1) / threads;
+        pool.emplace_back([&, t, n0, n1]() { st[t] = fn(n0, n1); });
+    }
+    for (auto& th : pool) th.join();
+    for (int s : st)
+        if (s != ORACLE_OK) return s;
+    return ORACLE_OK;
+}
+
+extern "C" int oracle_quantize(const void* x, int dtype, int64_t N, int64_t D, int32_t G,
+                               const uint8_t* bits, uint64_t seed, int64_t sample_base,
+                               uint8_t* packed, float* zmin, float* scale, int threads) {
+    if (N < 0 || D < 0 || G < 8 || G % 8 || sample_base < 0) return ORACLE_ERR_INVALID;
+    if (!bits_ok(bits, N)) return ORACLE_ERR_INVALID;
+    std::vector<int64_t> off((size_t)N + 1);
+    oracle_offsets(bits, N, D, G, off.data());
+    return fan_out(N, threads, [&](int64_t n0, int64_t n1) {
+        return quantize_range(x, dtype, n0, n1, D, G, bits, off.data(), seed, sample_base,
+                              packed, zmin, scale);
+    });
+}
+
+/* O10: h_hat = u_hat R / B + Z, evaluated as fmaf(code, scale, Z)
+ * with scale = RN(R/B) (one rounding; DESIGN reading 5). */
+extern "C" void oracle_dequantize_group(const uint8_t* seg, int32_t len, int32_t b,
+                                        float zmin, float scale, uint32_t* codes, float* out) {
+    for (int32_t k = 0; k < len; ++k) {
+        uint32_t code = 0;
+        for (int32_t t = 0; t < b; ++t) {
+            int64_t bit = (int64_t)k * b + t;
+            code |= (uint32_t)((seg[bit >> 3] >> (bit & 7)) & 1u) << t;
+        }
+        if (codes) codes[k] = code;
+        if (out) out[k] = std::fmaf((float)code, scale, zmin);
+    }
+}
+
+extern "C" int oracle_dequantize(const uint8_t* packed, const float* zmin, const float* scale,
+                                 const uint8_t* bits, int64_t N, int64_t D, int32_t G,
+                                 void* out, int out_dtype, int threads) {
+    if (N < 0 || D < 0 || G < 8 || G % 8) return ORACLE_ERR_INVALID;
+    if (!bits_ok(bits, N)) return ORACLE_ERR_INVALID;
+    int64_t ng = ceil_div(D, G);
+    std::vector<int64_t> off((size_t)N + 1);
+    oracle_offsets(bits, N, D, G, off.data());
+    return fan_out(N, threads, [&](int64_t n0, int64_t n1) {
+        std::vector<float> v(G);
+        for (int64_t n = n0; n < n1; ++n) {
+            int32_t b = bits[n];
+            for (int64_t i = 0; i < ng; ++i) {
+                int32_t len = (int32_t)std::min<int64_t>(G, D - i * G);
+                const uint8_t* seg = packed + off[n] + i * (int64_t)G * b / 8;
+                oracle_dequantize_group(seg, len, b, zmin[n * ng + i], scale[n * ng + i],
+                                        nullptr, v.data());
+                for (int32_t k = 0; k < len; ++k) {
+                    int64_t idx = n * D + i * G + k;
+                    if (out_dtype == ORACLE_F32)
+                        ((float*)out)[idx] = v[k];
+                    else
+                        ((uint16_t*)out)[idx] = to_bf16_rne(v[k]);
+                }
+            }
+        }
+        return ORACLE_OK;
+    });
+}
