@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""bench.py -- ActNN's hot path (per-group SR compressor + decompressor +
+per-sample greedy allocator) on B200, BASELINE.json's metric.
+
+A step = one pass of the whole hot path over one batch: for every tensor of
+the activation set, compress (group stats -> [all-gather of S, k > 1] ->
+greedy allocation -> SR quantise + pack) and decompress (unpack + dequantise).
+Default workload: C3 = the ResNet-50 activation set (107 tensors), batch 256
+per GPU, fp32, per-sample widths {1,2,4,8} averaging 2 bits.  Under torchrun
+each rank owns 256 samples (weak scaling) and the allocation is global over
+all ranks' samples.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5]
+  python bench.py --impl reference ...   # the CPU oracle on a bounded sample
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress+decompress GB/s and % HBM peak at 1/2/4/8 B200; codes bit-exact vs oracle"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="actnn", choices=["actnn", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+REASONS = [(0x4, "sw_power_cap"), (0x8, "hw_slowdown"), (0x20, "sw_thermal_slowdown"),
+           (0x40, "hw_thermal_slowdown"), (0x80, "hw_power_brake_slowdown"),
+           (0x2, "applications_clocks_setting"), (0x1, "gpu_idle")]
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons through NVML every 10 ms."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in REASONS:
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+# ------------------------------------------------------------------ helpers
+def algorithmic_bytes(layers, bits_host, s_in, s_out, mixed):
+    """Per-kernel algorithmic bytes (SURVEY §8(d) / DESIGN.md 'Roofline')."""
+    tot = {"stats": 0, "quantize": 0, "dequantize": 0}
+    for L, b in zip(layers, bits_host):
+        groups = L.N * L.ng
+        E = L.N * L.D
+        packed = int(b.long().sum()) * L.ng * 32
+        meta = 8 * groups
+        if mixed:
+            tot["stats"] += E * s_in + meta + 8 * L.N * (-(-L.ng // 32))
+            tot["quantize"] += E * s_in + meta + packed + meta + 9 * L.N
+        else:
+            tot["quantize"] += E * s_in + packed + meta + 9 * L.N
+        tot["dequantize"] += packed + meta + 9 * L.N + E * s_out
+    return tot
+
+
+def cpu_sample(wl, acts, args, target_s, seed_of, torch):
+    """Bounded CPU oracle run of the same workload: for every tensor of the
+    set, the first n_s samples go through stats -> heap allocation ->
+    quantize -> dequantize.  n_s is calibrated so the run takes ~target_s."""
+    import numpy as np
+    import oracle as O
+    from paper_2104_14129_b200 import workloads as W
+    cores = os.cpu_count() or 1
+
+    def run(n_s, xs_host):
+        t0 = time.perf_counter()
+        for li, (a, xh) in enumerate(zip(acts, xs_host)):
+            xh = xh[:n_s]
+            if wl.avg_bits is not None:
+                mn, mx = O.group_minmax(xh)
+                S = O.sensitivity(mn, mx)
+                bits = O.allocate_bits(S, int(wl.avg_bits * n_s))
+            else:
+                bits = np.full(n_s, wl.bits, np.uint8)
+            packed, zmin, scale, _ = O.quantize(xh, bits, seed_of(li), 0, threads=cores)
+            O.dequantize(packed, zmin, scale, bits, n_s, a.D,
+                         out_dtype=O.F32 if wl.dtype == "f32" else O.BF16, threads=cores)
+        return time.perf_counter() - t0
+
+    def host_inputs(n):
+        out = []
+        for li, a in enumerate(acts):
+            x = W.synth_activation(a, n, li, wl.dtype, "cpu")
+            if wl.dtype == "bf16":
+                out.append(x.view(torch.int16).numpy().view(np.uint16))
+            else:
+                out.append(x.numpy())
+        return out
+
+    xs1 = host_inputs(1)
+    t1 = run(1, xs1)
+    n_s = max(1, min(wl.N, int(target_s / max(t1, 1e-3))))
+    xs = host_inputs(n_s) if n_s > 1 else xs1
+    t = run(n_s, xs)
+    E = n_s * sum(a.D for a in acts)
+    s_in = 4 if wl.dtype == "f32" else 2
+    return {"value": E * s_in / t / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n_s} of {wl.N} samples of each of the {len(acts)} tensors "
+                      f"({E} elements, {E * s_in / 1e9:.2f} GB in), full compress+decompress "
+                      f"(stats, heap allocation, quantize, dequantize), {t:.1f} s"}, t
+
+
+def config_dict(wl, args, world, n_loc):
+    s_in = 4 if wl.dtype == "f32" else 2
+    E = n_loc * sum(a.D for a in wl.acts)
+    return {
+        "workload": f"{wl.name.upper()}: {wl.description}",
+        "tensors": len(wl.acts),
+        "samples_per_gpu": n_loc,
+        "global_batch": n_loc * world,
+        "elements_per_gpu_step": E,
+        "bytes_in_per_gpu_step": E * s_in,
+        "G": 256,
+        "bits": ("per-sample {1,2,4,8}, avg %.2f (greedy, global over ranks)" % wl.avg_bits)
+        if wl.avg_bits is not None else f"uniform {wl.bits}",
+        "parallelism": f"dp{world} (batch-sharded; all-gather of S per tensor)" if world > 1
+        else "dp1",
+        "l2": "inputs larger than L2: %.1f GB per step per GPU vs 126 MB L2" % (E * s_in / 1e9),
+    }
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    import torch
+    from paper_2104_14129_b200 import workloads as W
+    wl = W.workload(args.config)
+    world = args.gpus
+    n_loc = wl.N // world if args.config == "c5" else wl.N
+    per_step = max(1.0, min(5.0, 150.0 / max(1, args.steps + args.warmup)))
+    cb, _ = cpu_sample(wl, wl.acts, args, per_step, W.quant_seed, torch)
+    # steps: the same bounded sample, timed again K times after W warm-ups
+    import numpy as np
+    import oracle as O
+    n_s = int(cb["sample"].split()[1])
+    cores = os.cpu_count() or 1
+    xs = []
+    for li, a in enumerate(wl.acts):
+        x = W.synth_activation(a, n_s, li, wl.dtype, "cpu")
+        xs.append(x.view(torch.int16).numpy().view(np.uint16) if wl.dtype == "bf16" else x.numpy())
+
+    def step():
+        for li, (a, xh) in enumerate(zip(wl.acts, xs)):
+            if wl.avg_bits is not None:
+                mn, mx = O.group_minmax(xh)
+                bits = O.allocate_bits(O.sensitivity(mn, mx), int(wl.avg_bits * n_s))
+            else:
+                bits = np.full(n_s, wl.bits, np.uint8)
+            p, z, s, _ = O.quantize(xh, bits, W.quant_seed(li), 0, threads=cores)
+            O.dequantize(p, z, s, bits, n_s, a.D, out_dtype=O.F32 if wl.dtype == "f32" else O.BF16,
+                         threads=cores)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / max(1, args.steps)
+    s_in = 4 if wl.dtype == "f32" else 2
+    E = n_s * sum(a.D for a in wl.acts)
+    val = E * s_in / dt / 1e9
+    cb = dict(cb, value=val)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype,
+            "data": "synthetic (seeded ResNet-shaped activations, CPU generator)",
+            "config": config_dict(wl, args, world, n_loc), "cpu_baseline": cb,
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_14129_b200 as A
+    from paper_2104_14129_b200 import workloads as W
+    from paper_2104_14129_b200.plan import ActivationSetPlan
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    wl = W.workload(args.config)
+    n_loc = wl.N // world if args.config == "c5" else wl.N
+    n_total = n_loc * world
+    s_in = 4 if wl.dtype == "f32" else 2
+    tdt = torch.float32 if wl.dtype == "f32" else torch.bfloat16
+
+    # resident inputs (generated on the device, seeded per tensor and rank)
+    xs = []
+    for t, a in enumerate(wl.acts):
+        xs.append(W.synth_activation(a, n_loc, t + 100_000 * rank, wl.dtype, dev))
+    torch.cuda.synchronize()
+    gather = None
+    if world > 1:
+        def gather(S, S_loc):
+            dist.all_gather_into_tensor(S, S_loc)
+    plan = ActivationSetPlan(xs, [W.quant_seed(t) for t in range(len(wl.acts))],
+                             avg_bits=wl.avg_bits, bits=None if wl.avg_bits else wl.bits,
+                             n_total=n_total, sample_base=rank * n_loc, gather=gather)
+    max_numel = max(x.numel() for x in xs)
+    outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(2)]
+    out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
+    stream = torch.cuda.current_stream(dev)
+    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
+    nl = len(plan.layers)
+
+    def step(ev=None):
+        for i in range(nl):
+            plan.compress_layer(i, sp, None if ev is None else ev[i])
+        for i in range(nl):
+            plan.decompress_layer(i, outs[i & 1], out_dt, sp,
+                                  None if ev is None else ev[nl + i])
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+
+    # ---- headline: K steps, one event pair, max over ranks
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    E_loc = n_loc * sum(a.D for a in wl.acts)
+    value = world * E_loc * s_in / (ms_step * 1e-3) / 1e9
+
+    # ---- per-kernel breakdown: same steps with an event pair around every launch
+    kb = max(3, args.steps // 4)
+    evs = []
+    for _ in range(kb):
+        per = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nl)]
+        per += [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
+        evs.append(per)
+    barrier()
+    for s in range(kb):
+        step(evs[s])
+    barrier()
+    kt = {"stats": 0.0, "quantize": 0.0, "dequantize": 0.0}
+    tq = {"compress": 0.0, "decompress": 0.0}
+    for per in evs:
+        for i in range(nl):
+            if plan.mixed:
+                kt["stats"] += per[i][0].elapsed_time(per[i][1])
+            kt["quantize"] += per[i][2].elapsed_time(per[i][3])
+            kt["dequantize"] += per[nl + i][0].elapsed_time(per[nl + i][1])
+        tq["compress"] += per[0][0 if plan.mixed else 2].elapsed_time(per[nl - 1][3])
+        tq["decompress"] += per[nl][0].elapsed_time(per[2 * nl - 1][1])
+    for k in kt:
+        kt[k] /= kb
+    for k in tq:
+        tq[k] /= kb
+    bits_host = plan.bits_host()
+    alg = algorithmic_bytes(plan.layers, bits_host, s_in, s_in, plan.mixed)
+    peak, peak_src = hbm_peak()
+    dom = max(kt, key=lambda k: kt[k])
+    launches_dom = nl
+    ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": {"stats": "group_stats_kernel (K1)",
+                                           "quantize": "quantize_fast_kernel (K3)",
+                                           "dequantize": "dequantize_fast_kernel (K4)"}[dom],
+                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "peak_source": peak_src, "traffic": None,
+                "algorithmic_bytes_per_launch": alg[dom] / launches_dom,
+                "avg_launch_us": kt[dom] * 1e3 / launches_dom,
+                "per_kernel": {k: {"ms_per_step": kt[k], "share_of_step": kt[k] / ms_step,
+                                   "GBps": (alg[k] / (kt[k] * 1e-3) / 1e9) if kt[k] else None,
+                                   "frac": (alg[k] / (kt[k] * 1e-3) / 1e9 / peak) if kt[k] else None}
+                               for k in kt}}
+    total_alg = sum(alg.values())
+    avg_bits = [float(b.double().mean()) for b in bits_host]
+
+    # ---- e2e through the public API with host buffers (per-layer pipeline)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist,
+                      s_in, E_loc, barrier)
+
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak" if args.config != "c5" else "strong",
+            "vs_baseline": None, "dtype": wl.dtype,
+            "data": "synthetic (seeded ResNet-shaped activations generated on the GPU)",
+            "config": config_dict(wl, args, world, n_loc),
+            "compress_GBps": world * E_loc * s_in / (tq["compress"] * 1e-3) / 1e9,
+            "decompress_GBps": world * E_loc * s_in / (tq["decompress"] * 1e-3) / 1e9,
+            "hbm_frac_step": total_alg / (ms_step * 1e-3) / 1e9 / peak,
+            "roofline": roofline,
+            "gpu_launches": plan.launches_per_step() * args.steps,
+            "clocks": clk.summary(),
+            "avg_bits_realised": sum(avg_bits) / len(avg_bits)}
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cb, _ = cpu_sample(wl, wl.acts, args, args.cpu_seconds, W.quant_seed, torch)
+        line["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist, s_in,
+            E_loc, barrier):
+    """Host-pinned inputs copied in, compressed, decompressed and copied back
+    out every step (per-tensor pipeline over three streams)."""
+    import psutil
+    in_bytes = sum(x.numel() * x.element_size() for x in xs)
+    max_b = max(x.numel() * x.element_size() for x in xs)
+    if psutil.virtual_memory().available < (in_bytes + 3 * max_b) * 1.2 * world:
+        return {"value": None, "unit": "GB/s", "skipped": "not enough host memory for pinned "
+                "inputs", "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": in_bytes}
+    host_in = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in xs]
+    for h, x in zip(host_in, xs):
+        h.copy_(x)
+    host_out = [torch.empty(outs[0].numel(), dtype=outs[0].dtype, pin_memory=True)
+                for _ in range(3)]
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    nl = len(xs)
+    sample = max(1, int(os.environ.get("ACTNN_E2E_STEPS", args.e2e_steps)))
+
+    def e2e_step():
+        ev_in = [torch.cuda.Event() for _ in range(nl)]
+        ev_dq = [torch.cuda.Event() for _ in range(nl)]
+        ev_out = [torch.cuda.Event() for _ in range(nl)]
+        with torch.cuda.stream(h2d):
+            for i in range(nl):
+                xs[i].copy_(host_in[i], non_blocking=True)
+                ev_in[i].record(h2d)
+        for i in range(nl):
+            stream.wait_event(ev_in[i])
+            if i >= 2:
+                stream.wait_event(ev_out[i - 2])   # device out slot i&1 drained
+            plan.compress_layer(i, sp)
+            plan.decompress_layer(i, outs[i & 1], out_dt, sp)
+            ev_dq[i].record(stream)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_dq[i])
+                n = xs[i].numel()
+                host_out[i % 3][:n].copy_(outs[i & 1][:n], non_blocking=True)
+                ev_out[i].record(d2h)
+        stream.wait_stream(d2h)
+        stream.wait_stream(h2d)
+
+    e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(sample):
+        e2e_step()
+    e1.record()
+    barrier()
+    ms = e0.elapsed_time(e1) / sample
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"value": world * E_loc * s_in / (ms * 1e-3) / 1e9, "unit": "GB/s",
+            "ms_per_step": ms, "steps": sample,
+            "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": in_bytes,
+            "path": "pinned host -> H2D -> actnn_group_stats/allocate/quantize/dequantize "
+                    "(C ABI via plan) -> D2H pinned host, per-tensor pipelined on 3 streams"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

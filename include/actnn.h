@@ -1,0 +1,138 @@
+/*
+ * actnn.h -- C ABI of libactnn.so, the B200 (sm_100a) hot path of ActNN
+ * (Chen et al., "ActNN: Reducing Training Memory Footprint via 2-Bit
+ * Activation Compressed Training", ICML 2021, arXiv 2104.14129).
+ *
+ * Citations: P:<line> = PAPER.md line, S:<line> = SPEC.md line; "ACTNN-Q v1"
+ * is the arithmetic contract in DESIGN.md that
+ * makes the GPU codes bit-identical to the CPU oracle's.
+ *
+ * Conventions (every entry point):
+ *  - All array pointers are DEVICE pointers unless the name ends in _host.
+ *  - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL
+ *    = legacy default stream).  The library never allocates, frees,
+ *    synchronises or copies; the caller owns every buffer.  Reentrant.
+ *  - Arguments that can be checked on the host are checked before anything is
+ *    launched; a non-OK status launches nothing and actnn_last_error() returns
+ *    a thread-local message.  Launch failures return ACTNN_ERR_CUDA.
+ *  - N == 0 or D == 0 is a valid empty problem: OK, nothing launched.
+ *  - Device-resident data (bits[], off[], inputs) is not validated on the fast
+ *    path.  Inputs must be finite with |x| < 2^125 (SPEC "values finite",
+ *    S:125); bits[n] must lie in 1..8.  Setting ACTNN_CHECK=1 in the
+ *    environment makes every call synchronise and validate bits/off.
+ *  - Layouts: an activation is [N, D] row-major (sample n's flattened NCHW
+ *    tensor is row n).  Groups are G = 256 contiguous elements of one sample
+ *    ("partition its dimensions into groups h_ni"); ng = ceil(D/G); the
+ *    last group of a sample may be ragged.  Per-group arrays
+ *    (gmin, gmax, zmin, scale) are [N * ng], sample-major.
+ *  - Only G == 256 is supported in ABI v1 ("we set G = 256");
+ *    other G return ACTNN_ERR_UNSUPPORTED.
+ */
+#ifndef ACTNN_H
+#define ACTNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACTNN_ABI_VERSION 1
+
+typedef enum {
+    ACTNN_OK = 0,
+    ACTNN_ERR_INVALID = -1,      /* null pointer, negative size, bad enum, misalignment */
+    ACTNN_ERR_UNSUPPORTED = -2,  /* valid but outside ABI v1 (G != 256, packed not 16B-aligned) */
+    ACTNN_ERR_BUDGET = -3,       /* budget < N * (smallest allowed width) */
+    ACTNN_ERR_CUDA = -4,         /* kernel launch / CUDA runtime failure */
+    ACTNN_ERR_CHECK = -5         /* ACTNN_CHECK=1 found invalid device data */
+} actnn_status_t;
+
+typedef enum { ACTNN_F32 = 0, ACTNN_BF16 = 1 } actnn_dtype_t;
+
+/* level_mask: bit b set <=> width b allowed, b in 1..8. */
+#define ACTNN_LEVELS_POW2 ((1u << 1) | (1u << 2) | (1u << 4) | (1u << 8)) /* {1,2,4,8}: hot path */
+#define ACTNN_LEVELS_UNIT 0x1FEu /* 1..8: the paper's unit-step greedy */
+
+/* op ids for actnn_workspace_bytes */
+#define ACTNN_OP_GROUP_STATS 0
+#define ACTNN_OP_ALLOCATE_BITS 1
+
+/* Thread-local message describing the last non-OK status of this thread. */
+const char* actnn_last_error(void);
+
+/* ACTNN_ABI_VERSION of the loaded library. */
+int actnn_abi_version(void);
+
+/* Device workspace (bytes) `op` needs for an [N, D] problem; 0 = none. */
+size_t actnn_workspace_bytes(int op, int64_t N, int64_t D, int32_t G);
+
+/* Size in bytes of the packed code buffer: sum_n bits_host[n] * ng * G / 8
+ * (S:115).  bits_host == NULL gives the 8-bit upper bound 8*N*ng*G/8.
+ * Returns -1 on invalid arguments. */
+int64_t actnn_packed_bytes(int64_t N, int64_t D, int32_t G, const uint8_t* bits_host);
+
+/* Pass 1 of the mixed-precision path: for every
+ * group the canonical min Z and max M (signed zeros mapped to +0), and for
+ * every sample the range norm S_n = ||R_n||^2 = sum_i (M_ni - Z_ni)^2 in fp64,
+ * summed in the canonical order of ACTNN-Q v1 step O11 (32-group chunks, xor
+ * butterfly inside a chunk, chunks in order).  S_n is the sample's sensitivity
+ * w_n up to the per-sample gradient factor of Eq. 7.
+ *   x        [N, D] activations of dtype dt
+ *   gmin/gmax [N*ng] fp32 outputs;  sens [N] fp64 output
+ *   ws       >= actnn_workspace_bytes(ACTNN_OP_GROUP_STATS, N, D, G) bytes, 8B-aligned */
+actnn_status_t actnn_group_stats(const void* x, actnn_dtype_t dt, int64_t N, int64_t D, int32_t G,
+                                 float* gmin, float* gmax, double* sens, void* ws,
+                                 size_t ws_bytes, void* stream);
+
+/* Stage 1 of the run-time adaptation (Prob. 8 at P:541-547 for one
+ * layer): the paper's greedy, computed on the device in one CTA.
+ * w_n = sens[n] * (gscale ? gscale[n] : 1).  Every sample starts at the widest
+ * allowed width; moves (one allowed width down) are applied in ascending
+ * (w_n * slope_c, n, c) order, slope_c = (1/B_{c+1}^2 - 1/B_c^2) / freed bits,
+ * until sum_n bits[n] <= budget.  Bit-identical to the oracle's binary heap.
+ *   sens, gscale [N] fp64, finite and >= 0;  budget: max sum_n bits[n]
+ *   level_mask: allowed widths (ACTNN_LEVELS_POW2 on the hot path)
+ *   D, G: used for the offsets only
+ *   bits [N] u8 output;  off [N+1] i64 output: off[0] = 0,
+ *   off[n+1] = off[n] + bits[n] * ng * G / 8 (byte offsets into `packed`)
+ *   ws: unused in v1 (pass NULL, 0). */
+actnn_status_t actnn_allocate_bits(const double* sens, const double* gscale, int64_t N,
+                                   int64_t budget, uint32_t level_mask, int64_t D, int32_t G,
+                                   uint8_t* bits, int64_t* off, void* ws, size_t ws_bytes,
+                                   void* stream);
+
+/* Uniform widths (optimization level L2): bits[n] = b for all n and
+ * the matching off[N+1].  b in 1..8. */
+actnn_status_t actnn_uniform_bits(int64_t N, int64_t D, int32_t G, int32_t b, uint8_t* bits,
+                                  int64_t* off, void* stream);
+
+/* Compressor: per group Z = min, R = max - min,
+ * scale = RN(R/B), u_bar = B (h - Z)/R in 14-bit fixed point, unbiased
+ * stochastic rounding with Philox4x32-10(ctr = e >> 3, key = seed) where
+ * e = (sample_base + n) * D + d is the element's global index, and LSB-first
+ * packing of the b_n-bit codes.
+ *   x [N, D] dtype dt;  bits [N], off [N+1] as produced by actnn_allocate_bits
+ *   (sample n's bytes start at packed + off[n] - off[0], so a rank may pass a
+ *   slice of a global off[] array);  sample_base: global index of this shard's
+ *   first sample (ranks of a batch-sharded job pass r * N_local);
+ *   gmin/gmax: NULL => one pass computing min/max in-kernel, else the
+ *   actnn_group_stats outputs (results are identical either way);
+ *   packed: off[N] - off[0] bytes, 16-byte aligned;  zmin/scale [N*ng] fp32. */
+actnn_status_t actnn_quantize(const void* x, actnn_dtype_t dt, int64_t N, int64_t D, int32_t G,
+                              const uint8_t* bits, const int64_t* off, uint64_t seed,
+                              int64_t sample_base, const float* gmin, const float* gmax,
+                              uint8_t* packed, float* zmin, float* scale, void* stream);
+
+/* Decompressor: h_hat = code * scale + Z with a single rounding
+ * (fmaf); bf16 output is RNE(h_hat).  Buffers as for actnn_quantize;
+ * out [N, D] of dtype out_dt. */
+actnn_status_t actnn_dequantize(const uint8_t* packed, const float* zmin, const float* scale,
+                                const uint8_t* bits, const int64_t* off, int64_t N, int64_t D,
+                                int32_t G, void* out, actnn_dtype_t out_dt, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACTNN_H */

@@ -1,0 +1,223 @@
+"""Python face of the ActNN hot path: thin wrappers over the C ABI.
+
+Each function allocates its outputs as torch tensors (PyTorch is used only for
+device memory and streams), passes ``data_ptr()``s and the current CUDA stream
+to ``libactnn.so``, and checks the status.  No arithmetic of the method
+happens here: group statistics, allocation, quantisation and dequantisation
+all run in the sm_100a kernels.  Inputs must be CUDA tensors; there is no CPU
+fallback.
+
+Names follow the paper (P = PAPER.md): quantize/dequantize (§4.1),
+allocate_bits (stage 1 of §4.3), group_stats (the ||R_n||^2 factor
+of the sensitivity, Eq. 7-8).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Callable, Optional, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import ActnnError  # noqa: F401
+
+G = 256
+F32, BF16 = 0, 1
+LEVELS_POW2 = (1 << 1) | (1 << 2) | (1 << 4) | (1 << 8)
+LEVELS_UNIT = 0x1FE
+OP_GROUP_STATS = 0
+
+
+def library_path() -> str:
+    return _lib.LIB_PATH
+
+
+def abi_version() -> int:
+    return int(_lib.load().actnn_abi_version())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(dev: torch.device):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return F32
+    if dt == torch.bfloat16:
+        return BF16
+    raise ActnnError(-1, f"unsupported dtype {dt} (fp32 or bf16)")
+
+
+def _as_2d(x: torch.Tensor) -> torch.Tensor:
+    if not x.is_cuda:
+        raise ActnnError(-1, "actnn needs CUDA tensors (there is no CPU fallback)")
+    if not x.is_contiguous():
+        raise ActnnError(-1, "actnn needs a contiguous [N, ...] activation")
+    N = x.shape[0] if x.dim() > 0 else 1
+    return x.reshape(N, -1)
+
+
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def packed_bytes(N: int, D: int, bits_host=None) -> int:
+    """Bytes of the packed stream: sum_n b_n * ceil(D/G) * G / 8; None = 8-bit bound."""
+    arr = None
+    if bits_host is not None:
+        import numpy as np
+        arr = np.ascontiguousarray(bits_host, dtype=np.uint8)
+    v = _lib.load().actnn_packed_bytes(N, D, G, None if arr is None else arr.ctypes.data_as(
+        ctypes.c_void_p))
+    if v < 0:
+        raise ActnnError(-1, "invalid arguments to actnn_packed_bytes")
+    return int(v)
+
+
+@dataclass
+class Packed:
+    """A compressed activation (the saved context of P:578-592)."""
+    packed: torch.Tensor      # uint8 code stream, sample n at off[n] - off[0]
+    zmin: torch.Tensor        # fp32 [N * ng]  zero points Z_ni
+    scale: torch.Tensor       # fp32 [N * ng]  R_ni / B_n
+    bits: torch.Tensor        # uint8 [N]      b_n
+    off: torch.Tensor         # int64 [N + 1]  byte offsets
+    shape: Tuple[int, ...]    # original activation shape
+    dtype: torch.dtype        # original activation dtype
+    seed: int
+    sample_base: int
+
+    @property
+    def N(self) -> int:
+        return self.shape[0]
+
+    @property
+    def D(self) -> int:
+        n = 1
+        for s in self.shape[1:]:
+            n *= s
+        return n
+
+    def nbytes(self) -> int:
+        return (self.packed.numel() + 4 * self.zmin.numel() + 4 * self.scale.numel()
+                + self.bits.numel() + 8 * self.off.numel())
+
+
+def group_stats(x: torch.Tensor, sens_out: Optional[torch.Tensor] = None):
+    """Per-group canonical (min, max) and per-sample S_n = ||R_n||^2 (fp64).
+
+    ``sens_out`` (fp64 [N], e.g. a slice of a zero-padded global vector for
+    the sharded path) receives S when given."""
+    x2 = _as_2d(x)
+    N, D = x2.shape
+    ng = ceil_div(D, G)
+    dev = x2.device
+    gmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
+    gmax = torch.empty(N * ng, dtype=torch.float32, device=dev)
+    sens = sens_out if sens_out is not None else torch.empty(N, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    wsb = int(lib.actnn_workspace_bytes(OP_GROUP_STATS, N, D, G))
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+    _lib.check(lib.actnn_group_stats(_ptr(x2), _dtype_code(x2.dtype), N, D, G, _ptr(gmin),
+                                     _ptr(gmax), _ptr(sens), _ptr(ws), ws.numel(), _stream(dev)))
+    return gmin, gmax, sens
+
+
+def allocate_bits(sens: torch.Tensor, budget: int, D: int, level_mask: int = LEVELS_POW2,
+                  gscale: Optional[torch.Tensor] = None):
+    """Stage-1 greedy on the device -> (bits u8 [N], off i64 [N+1])."""
+    if not sens.is_cuda or sens.dtype != torch.float64:
+        raise ActnnError(-1, "sens must be a CUDA fp64 tensor")
+    N = sens.numel()
+    dev = sens.device
+    bits = torch.empty(N, dtype=torch.uint8, device=dev)
+    off = torch.empty(N + 1, dtype=torch.int64, device=dev)
+    _lib.check(_lib.load().actnn_allocate_bits(_ptr(sens.contiguous()), _ptr(gscale), N,
+                                               int(budget), level_mask, D, G, _ptr(bits),
+                                               _ptr(off), None, 0, _stream(dev)))
+    return bits, off
+
+
+def uniform_bits(N: int, D: int, b: int, device) -> Tuple[torch.Tensor, torch.Tensor]:
+    dev = torch.device(device)
+    bits = torch.empty(N, dtype=torch.uint8, device=dev)
+    off = torch.empty(N + 1, dtype=torch.int64, device=dev)
+    _lib.check(_lib.load().actnn_uniform_bits(N, D, G, b, _ptr(bits), _ptr(off), _stream(dev)))
+    return bits, off
+
+
+def quantize(x: torch.Tensor, bits: torch.Tensor, off: torch.Tensor, seed: int,
+             sample_base: int = 0, gmin: Optional[torch.Tensor] = None,
+             gmax: Optional[torch.Tensor] = None, packed: Optional[torch.Tensor] = None,
+             zmin: Optional[torch.Tensor] = None, scale: Optional[torch.Tensor] = None,
+             packed_nbytes: Optional[int] = None) -> Packed:
+    """Compressor: per-group SR quantisation + packing.
+
+    ``packed`` defaults to the 8-bit upper bound (bits live on the device);
+    pass ``packed_nbytes`` (e.g. read back from off[N]) to size it exactly."""
+    x2 = _as_2d(x)
+    N, D = x2.shape
+    ng = ceil_div(D, G)
+    dev = x2.device
+    if packed is None:
+        nbytes = packed_nbytes if packed_nbytes is not None else N * ng * G
+        packed = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    if zmin is None:
+        zmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
+    if scale is None:
+        scale = torch.empty(N * ng, dtype=torch.float32, device=dev)
+    _lib.check(_lib.load().actnn_quantize(
+        _ptr(x2), _dtype_code(x2.dtype), N, D, G, _ptr(bits), _ptr(off),
+        ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), sample_base, _ptr(gmin), _ptr(gmax),
+        _ptr(packed), _ptr(zmin), _ptr(scale), _stream(dev)))
+    return Packed(packed, zmin, scale, bits, off, tuple(x.shape), x.dtype, seed, sample_base)
+
+
+def dequantize(p: Packed, out: Optional[torch.Tensor] = None,
+               out_dtype: Optional[torch.dtype] = None) -> torch.Tensor:
+    """Decompressor into a tensor of the original shape."""
+    dev = p.packed.device
+    if out is None:
+        out = torch.empty(p.shape, dtype=out_dtype or p.dtype, device=dev)
+    _lib.check(_lib.load().actnn_dequantize(
+        _ptr(p.packed), _ptr(p.zmin), _ptr(p.scale), _ptr(p.bits), _ptr(p.off), p.N, p.D, G,
+        _ptr(out), _dtype_code(out.dtype), _stream(dev)))
+    return out
+
+
+def compress(x: torch.Tensor, seed: int, bits: Optional[int] = None,
+             avg_bits: Optional[float] = None, level_mask: int = LEVELS_POW2,
+             sample_base: int = 0, gscale: Optional[torch.Tensor] = None,
+             sens_allreduce: Optional[Callable[[torch.Tensor], torch.Tensor]] = None,
+             n_total: Optional[int] = None) -> Packed:
+    """One layer's compress call.
+
+    bits=b: uniform b-bit (optimization level L2, single pass).
+    avg_bits=a: per-sample mixed precision (L2.5): group_stats ->
+    [sens_allreduce hook: sums the zero-padded S across ranks] -> greedy
+    allocation with budget floor(a * N_total) -> quantize with the stats."""
+    x2 = _as_2d(x)
+    N, D = x2.shape
+    if bits is not None:
+        b, o = uniform_bits(N, D, bits, x2.device)
+        return quantize(x, b, o, seed, sample_base)
+    if avg_bits is None:
+        raise ActnnError(-1, "compress needs bits= or avg_bits=")
+    nt = n_total if n_total is not None else N
+    S = torch.zeros(nt, dtype=torch.float64, device=x2.device)
+    gmin, gmax, _ = group_stats(x, sens_out=S[sample_base:sample_base + N] if nt != N else S)
+    if sens_allreduce is not None:
+        S = sens_allreduce(S)
+    budget = int(avg_bits * nt)
+    bits_g, off_g = allocate_bits(S, budget, D, level_mask, gscale)
+    lo = sample_base if nt != N else 0
+    return quantize(x, bits_g[lo:lo + N], off_g[lo:lo + N + 1], seed, sample_base, gmin, gmax)
+
+
+def decompress(p: Packed, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    return dequantize(p, out)

@@ -1,0 +1,310 @@
+// abi.cu -- the C ABI of libactnn.so (include/actnn.h): host-side argument
+// checks, launch-shape selection and error reporting.  No allocation, no
+// synchronisation (except the opt-in ACTNN_CHECK=1 debug mode), no copies.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/actnn.h"
+#include "launch.h"
+
+namespace actnn {
+
+namespace {
+thread_local char g_err[512] = "";
+
+actnn_status_t fail(actnn_status_t st, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+actnn_status_t cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return ACTNN_OK;
+    return fail(ACTNN_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool check_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* v = std::getenv("ACTNN_CHECK");
+        mode = (v && v[0] && v[0] != '0') ? 1 : 0;
+    }
+    return mode == 1;
+}
+
+bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ACTNN_CHECK=1: synchronise and validate the device-resident widths/offsets.
+actnn_status_t debug_validate(const uint8_t* bits, const int64_t* off, int64_t N, int64_t ng,
+                              cudaStream_t s) {
+    if (!check_mode()) return ACTNN_OK;
+    std::vector<uint8_t> hb((size_t)N);
+    std::vector<int64_t> ho((size_t)N + 1);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMemcpy(hb.data(), bits, (size_t)N, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(ho.data(), off, sizeof(int64_t) * (size_t)(N + 1), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "ACTNN_CHECK copy");
+    for (int64_t n = 0; n < N; ++n) {
+        if (hb[n] < 1 || hb[n] > 8)
+            return fail(ACTNN_ERR_CHECK, "ACTNN_CHECK: bits[%lld] = %d outside 1..8", (long long)n,
+                        (int)hb[n]);
+        if (ho[n + 1] - ho[n] != (int64_t)hb[n] * ng * 32)
+            return fail(ACTNN_ERR_CHECK, "ACTNN_CHECK: off[%lld..%lld] inconsistent with bits",
+                        (long long)n, (long long)n + 1);
+    }
+    return ACTNN_OK;
+}
+
+actnn_status_t post_launch(cudaError_t e, const char* what, cudaStream_t s) {
+    if (e != cudaSuccess) return cuda_status(e, what);
+    if (check_mode()) return cuda_status(cudaStreamSynchronize(s), what);
+    return ACTNN_OK;
+}
+
+struct DeviceInfo {
+    int sms = 0;
+};
+std::mutex g_dev_mu;
+std::vector<DeviceInfo> g_dev;
+}  // namespace
+
+int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+        if (g_dev[dev].sms == 0)
+            cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+        sms = g_dev[dev].sms;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem) != cudaSuccess ||
+        occ < 1)
+        occ = 1;
+    const int64_t cap = (int64_t)sms * occ;
+    int64_t g = work_blocks < cap ? work_blocks : cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace actnn
+
+using namespace actnn;
+
+extern "C" {
+
+const char* actnn_last_error(void) { return g_err; }
+
+int actnn_abi_version(void) { return ACTNN_ABI_VERSION; }
+
+size_t actnn_workspace_bytes(int op, int64_t N, int64_t D, int32_t G) {
+    if (N <= 0 || D <= 0 || G <= 0) return 0;
+    if (op == ACTNN_OP_GROUP_STATS) return (size_t)(N * ceil_div(ceil_div(D, G), 32)) * 8;
+    return 0;
+}
+
+int64_t actnn_packed_bytes(int64_t N, int64_t D, int32_t G, const uint8_t* bits_host) {
+    if (N < 0 || D < 0 || G <= 0 || G % 8) return -1;
+    const int64_t ng = ceil_div(D, G);
+    if (!bits_host) return N * ng * G;  // 8-bit bound
+    int64_t s = 0;
+    for (int64_t n = 0; n < N; ++n) {
+        if (bits_host[n] < 1 || bits_host[n] > 8) return -1;
+        s += (int64_t)bits_host[n] * ng * G / 8;
+    }
+    return s;
+}
+
+static actnn_status_t common_checks(int64_t N, int64_t D, int32_t G) {
+    if (N < 0 || D < 0) return fail(ACTNN_ERR_INVALID, "negative size N=%lld D=%lld",
+                                    (long long)N, (long long)D);
+    if (G != 256) return fail(ACTNN_ERR_UNSUPPORTED, "G=%d unsupported (ABI v1: G=256)", G);
+    return ACTNN_OK;
+}
+
+static bool dtype_ok(int dt) { return dt == ACTNN_F32 || dt == ACTNN_BF16; }
+
+actnn_status_t actnn_group_stats(const void* x, actnn_dtype_t dt, int64_t N, int64_t D, int32_t G,
+                                 float* gmin, float* gmax, double* sens, void* ws,
+                                 size_t ws_bytes, void* stream) {
+    actnn_status_t st = common_checks(N, D, G);
+    if (st) return st;
+    if (!dtype_ok(dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)dt);
+    if (N == 0 || D == 0) return ACTNN_OK;
+    if (!x || !gmin || !gmax || !sens || !ws)
+        return fail(ACTNN_ERR_INVALID, "actnn_group_stats: null pointer");
+    const size_t es = dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(x, es) || !aligned(gmin, 4) || !aligned(gmax, 4) || !aligned(sens, 8) ||
+        !aligned(ws, 8))
+        return fail(ACTNN_ERR_INVALID, "actnn_group_stats: misaligned pointer");
+    if (ws_bytes < actnn_workspace_bytes(ACTNN_OP_GROUP_STATS, N, D, G))
+        return fail(ACTNN_ERR_INVALID, "actnn_group_stats: workspace %zu < %zu bytes", ws_bytes,
+                    actnn_workspace_bytes(ACTNN_OP_GROUP_STATS, N, D, G));
+    StatsArgs a;
+    a.x = x;
+    a.dt = (int)dt;
+    a.N = N;
+    a.D = D;
+    a.ng = ceil_div(D, G);
+    a.nch = ceil_div(a.ng, 32);
+    a.gmin = gmin;
+    a.gmax = gmax;
+    a.sens = sens;
+    a.T = static_cast<double*>(ws);
+    a.fast = (D % G == 0) && aligned(x, dt == ACTNN_F32 ? 32 : 16);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_group_stats(a, s), "actnn_group_stats", s);
+}
+
+static actnn_status_t levels_from_mask(uint32_t mask, int* L, int* m) {
+    if (mask == 0 || (mask & ~0x1FEu))
+        return fail(ACTNN_ERR_INVALID, "level_mask 0x%x must be a non-empty subset of bits 1..8",
+                    mask);
+    *m = 0;
+    for (int b = 8; b >= 1; --b)
+        if (mask & (1u << b)) L[(*m)++] = b;
+    return ACTNN_OK;
+}
+
+actnn_status_t actnn_allocate_bits(const double* sens, const double* gscale, int64_t N,
+                                   int64_t budget, uint32_t level_mask, int64_t D, int32_t G,
+                                   uint8_t* bits, int64_t* off, void* ws, size_t ws_bytes,
+                                   void* stream) {
+    (void)ws;
+    (void)ws_bytes;
+    actnn_status_t st = common_checks(N, D, G);
+    if (st) return st;
+    AllocArgs a;
+    std::memset(&a, 0, sizeof(a));
+    st = levels_from_mask(level_mask, a.L, &a.m);
+    if (st) return st;
+    if (budget < N * (int64_t)a.L[a.m - 1])
+        return fail(ACTNN_ERR_BUDGET, "budget %lld < N * %d = %lld (infeasible)",
+                    (long long)budget, a.L[a.m - 1], (long long)(N * a.L[a.m - 1]));
+    if (N == 0) {
+        if (!off) return fail(ACTNN_ERR_INVALID, "actnn_allocate_bits: null off");
+        return cuda_status(cudaMemsetAsync(off, 0, sizeof(int64_t), (cudaStream_t)stream),
+                           "actnn_allocate_bits");
+    }
+    if (!sens || !bits || !off) return fail(ACTNN_ERR_INVALID, "actnn_allocate_bits: null pointer");
+    if (!aligned(sens, 8) || !aligned(off, 8) || (gscale && !aligned(gscale, 8)))
+        return fail(ACTNN_ERR_INVALID, "actnn_allocate_bits: misaligned pointer");
+    // per-bit variance slope of each move (Eq. 8 with B = 2^b - 1): the move
+    // from L[c] to L[c+1] raises w/B^2 by w (1/B_{c+1}^2 - 1/B_c^2) and frees
+    // L[c] - L[c+1] bits (DESIGN reading 9).
+    for (int c = 0; c + 1 < a.m; ++c) {
+        const double Bh = (double)((1 << a.L[c]) - 1), Bl = (double)((1 << a.L[c + 1]) - 1);
+        const double fh = 1.0 / (Bh * Bh), fl = 1.0 / (Bl * Bl);
+        a.freed[c] = a.L[c] - a.L[c + 1];
+        a.slope[c] = (fl - fh) / (double)a.freed[c];
+    }
+    a.sens = sens;
+    a.gscale = gscale;
+    a.N = N;
+    a.need = N * (int64_t)a.L[0] - budget;
+    a.unit = ceil_div(D, G) * G / 8;
+    a.bits = bits;
+    a.off = off;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_allocate(a, s), "actnn_allocate_bits", s);
+}
+
+actnn_status_t actnn_uniform_bits(int64_t N, int64_t D, int32_t G, int32_t b, uint8_t* bits,
+                                  int64_t* off, void* stream) {
+    actnn_status_t st = common_checks(N, D, G);
+    if (st) return st;
+    if (b < 1 || b > 8) return fail(ACTNN_ERR_INVALID, "width %d outside 1..8", b);
+    if (!off || (N > 0 && !bits)) return fail(ACTNN_ERR_INVALID, "actnn_uniform_bits: null pointer");
+    if (!aligned(off, 8)) return fail(ACTNN_ERR_INVALID, "actnn_uniform_bits: misaligned off");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_uniform_bits(N, b, ceil_div(D, G) * G / 8, bits, off, s),
+                       "actnn_uniform_bits", s);
+}
+
+actnn_status_t actnn_quantize(const void* x, actnn_dtype_t dt, int64_t N, int64_t D, int32_t G,
+                              const uint8_t* bits, const int64_t* off, uint64_t seed,
+                              int64_t sample_base, const float* gmin, const float* gmax,
+                              uint8_t* packed, float* zmin, float* scale, void* stream) {
+    actnn_status_t st = common_checks(N, D, G);
+    if (st) return st;
+    if (!dtype_ok(dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)dt);
+    if (sample_base < 0) return fail(ACTNN_ERR_INVALID, "negative sample_base");
+    if (N == 0 || D == 0) return ACTNN_OK;
+    if (!x || !bits || !off || !packed || !zmin || !scale)
+        return fail(ACTNN_ERR_INVALID, "actnn_quantize: null pointer");
+    if ((gmin == nullptr) != (gmax == nullptr))
+        return fail(ACTNN_ERR_INVALID, "actnn_quantize: gmin and gmax must both be set or NULL");
+    const size_t es = dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(x, es) || !aligned(off, 8) || !aligned(zmin, 4) || !aligned(scale, 4) ||
+        (gmin && (!aligned(gmin, 4) || !aligned(gmax, 4))))
+        return fail(ACTNN_ERR_INVALID, "actnn_quantize: misaligned pointer");
+    if (!aligned(packed, 16))
+        return fail(ACTNN_ERR_UNSUPPORTED, "actnn_quantize: packed must be 16-byte aligned");
+    const int64_t ng = ceil_div(D, G);
+    st = debug_validate(bits, off, N, ng, (cudaStream_t)stream);
+    if (st) return st;
+    QuantArgs a;
+    a.x = x;
+    a.dt = (int)dt;
+    a.N = N;
+    a.D = D;
+    a.ng = ng;
+    a.bits = bits;
+    a.off = off;
+    a.seed = seed;
+    a.sample_base = sample_base;
+    a.gmin = gmin;
+    a.gmax = gmax;
+    a.packed = packed;
+    a.zmin = zmin;
+    a.scale = scale;
+    a.fast = (D % G == 0) && aligned(x, dt == ACTNN_F32 ? 32 : 16);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_quantize(a, s), "actnn_quantize", s);
+}
+
+actnn_status_t actnn_dequantize(const uint8_t* packed, const float* zmin, const float* scale,
+                                const uint8_t* bits, const int64_t* off, int64_t N, int64_t D,
+                                int32_t G, void* out, actnn_dtype_t out_dt, void* stream) {
+    actnn_status_t st = common_checks(N, D, G);
+    if (st) return st;
+    if (!dtype_ok(out_dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)out_dt);
+    if (N == 0 || D == 0) return ACTNN_OK;
+    if (!packed || !zmin || !scale || !bits || !off || !out)
+        return fail(ACTNN_ERR_INVALID, "actnn_dequantize: null pointer");
+    const size_t es = out_dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(out, es) || !aligned(off, 8) || !aligned(zmin, 4) || !aligned(scale, 4))
+        return fail(ACTNN_ERR_INVALID, "actnn_dequantize: misaligned pointer");
+    if (!aligned(packed, 16))
+        return fail(ACTNN_ERR_UNSUPPORTED, "actnn_dequantize: packed must be 16-byte aligned");
+    const int64_t ng = ceil_div(D, G);
+    st = debug_validate(bits, off, N, ng, (cudaStream_t)stream);
+    if (st) return st;
+    DequantArgs a;
+    a.packed = packed;
+    a.zmin = zmin;
+    a.scale = scale;
+    a.bits = bits;
+    a.off = off;
+    a.N = N;
+    a.D = D;
+    a.ng = ng;
+    a.out = out;
+    a.out_dt = (int)out_dt;
+    a.fast = (D % G == 0) && aligned(out, out_dt == ACTNN_F32 ? 32 : 16);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_dequantize(a, s), "actnn_dequantize", s);
+}
+
+}  // extern "C"

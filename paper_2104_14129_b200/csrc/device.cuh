@@ -1,0 +1,173 @@
+// device.cuh -- sm_100a building blocks shared by the ActNN kernels.
+//
+// Independent of oracle/ (no shared code).  Floating-point steps use explicit
+// round-to-nearest intrinsics and the library is compiled with -fmad=false and
+// without -ftz / fast-math so that every rounding is the one ACTNN-Q v1 fixes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace actnn {
+
+constexpr int kG = 256;            // group size ("we set G = 256")
+constexpr int kWarp = 32;
+constexpr int kElemsPerLane = 8;   // kG / kWarp: one Philox call per lane per group
+constexpr int kChunk = 32;         // groups per tile = one group per lane for metadata
+
+// -------------------------------------------------------------------- Philox
+// Philox4x32-10 (Salmon et al., SC'11): multipliers 0xD2511F53 / 0xCD9E8D57,
+// Weyl key increments 0x9E3779B9 / 0xBB67AE85, key bumped between rounds.
+// The counter words 2,3 are always 0 in ACTNN-Q v1 (ctr = e >> 3 is 64-bit).
+// The key depends only on the seed, so ptxas keeps the round keys in uniform
+// registers; each round is 2 IMAD.WIDE.U32 + 2 LOP3.
+struct Philox4 {
+    uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t k0,
+                                                 uint32_t k1) {
+    uint32_t c2 = 0u, c3 = 0u;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint32_t lo0 = 0xD2511F53u * c0;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0;
+        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return Philox4{c0, c1, c2, c3};
+}
+
+// 14-bit draw of element j (0..7) of an 8-element Philox block: 16-bit lane j.
+__device__ __forceinline__ uint32_t rnd14(const Philox4& o, int j) {
+    const uint32_t w = (j >> 1) == 0 ? o.x : (j >> 1) == 1 ? o.y : (j >> 1) == 2 ? o.z : o.w;
+    return ((j & 1) ? (w >> 16) : w) & 0x3FFFu;
+}
+
+// ------------------------------------------------------------- warp helpers
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ---------------------------------------------------------------- loads
+// 8 consecutive elements (32 B fp32 / 16 B bf16) of a lane, widened to fp32.
+// fp32 uses the sm_100 256-bit load (LDG.E.256): one instruction moves a
+// lane's whole 8-element slice, so every warp load covers 1 KB = 32 full
+// sectors.  .nc: read-only path; L1::no_allocate: streamed once per kernel
+// (L2 keeps the default policy so the mixed path's second pass can hit L2).
+struct F32Tag {};
+struct BF16Tag {};
+
+__device__ __forceinline__ void load8(const float* p, float v[8]) {
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+          "=f"(v[7])
+        : "l"(p));
+}
+
+__device__ __forceinline__ void load8(const uint16_t* p, float v[8]) {
+    uint32_t a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "l"(p));
+    // bf16 -> fp32 is exact: the bf16 bits are the high half of the fp32 bits
+    v[0] = __uint_as_float(a << 16);
+    v[1] = __uint_as_float(a & 0xFFFF0000u);
+    v[2] = __uint_as_float(b << 16);
+    v[3] = __uint_as_float(b & 0xFFFF0000u);
+    v[4] = __uint_as_float(c << 16);
+    v[5] = __uint_as_float(c & 0xFFFF0000u);
+    v[6] = __uint_as_float(d << 16);
+    v[7] = __uint_as_float(d & 0xFFFF0000u);
+}
+
+__device__ __forceinline__ float load1(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float load1(const uint16_t* p) {
+    return __uint_as_float((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p)) << 16);
+}
+
+// ---------------------------------------------------------------- stores
+__device__ __forceinline__ void store8(float* p, const float v[8]) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+
+// RNE fp32 -> bf16 pair (cvt.rn.bf16x2.f32); low half = first element.
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+__device__ __forceinline__ void store8(uint16_t* p, const float v[8]) {
+    const uint32_t a = pack_bf16x2(v[0], v[1]);
+    const uint32_t b = pack_bf16x2(v[2], v[3]);
+    const uint32_t c = pack_bf16x2(v[4], v[5]);
+    const uint32_t d = pack_bf16x2(v[6], v[7]);
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ void store1(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store1(uint16_t* p, float v) {
+    *p = (uint16_t)(pack_bf16x2(v, 0.0f) & 0xFFFFu);
+}
+
+// ------------------------------------------------------ quantiser constants
+// ACTNN-Q v1 O3-O4 for one group from its exact min/max:
+// Z, M canonical (+0 for signed zeros), R = RN(M - Z), scale = RN(R / B),
+// inv14 = RN(B / R) * 2^14 (0 for the degenerate R < 2^-96).
+struct GroupConst {
+    float Z, scale, inv14;
+};
+
+__device__ __forceinline__ GroupConst group_const(float mn, float mx, int b) {
+    GroupConst c;
+    const float Z = __fadd_rn(mn, 0.0f);
+    const float M = __fadd_rn(mx, 0.0f);
+    const float R = __fsub_rn(M, Z);
+    const float Bf = (float)((1u << b) - 1u);
+    c.Z = Z;
+    c.scale = __fdiv_rn(R, Bf);
+    c.inv14 = (R < 0x1p-96f) ? 0.0f : __fmul_rn(__fdiv_rn(Bf, R), 16384.0f);
+    return c;
+}
+
+// ACTNN-Q v1 O5 + O7: q = RNE((h - Z) * inv14) as an integer in [0, B*2^14],
+// obtained exactly from one fma against 1.5*2^23 (the sum stays in
+// [2^23, 2^24) where the ulp is 1; the constant is even so ties agree with
+// RNE), then code = (q + r) >> 14 (stochastic rounding).
+__device__ __forceinline__ uint32_t sr_code(float h, float Z, float inv14, uint32_t r14) {
+    const float d = __fsub_rn(h, Z);
+    const float t = __fmaf_rn(d, inv14, 12582912.0f);
+    return (__float_as_uint(t) - 0x4B400000u + r14) >> 14;
+}
+
+// ACTNN-Q v1 O10: h_hat = fmaf((float)code, scale, Z); (float)code is exact
+// via the 2^23 magic (code < 2^8).
+__device__ __forceinline__ float dequant1(uint32_t code, float scale, float Z) {
+    const float c = __fsub_rn(__uint_as_float(0x4B000000u | code), 8388608.0f);
+    return __fmaf_rn(c, scale, Z);
+}
+
+}  // namespace actnn

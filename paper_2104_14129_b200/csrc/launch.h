@@ -1,0 +1,72 @@
+// launch.h -- internal host launchers (C++ linkage, not exported).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace actnn {
+
+struct QuantArgs {
+    const void* x;
+    int dt;  // 0 f32, 1 bf16
+    int64_t N, D, ng;
+    const uint8_t* bits;
+    const int64_t* off;
+    uint64_t seed;
+    int64_t sample_base;
+    const float* gmin;
+    const float* gmax;
+    uint8_t* packed;
+    float* zmin;
+    float* scale;
+    bool fast;  // D % 256 == 0 and x aligned for vector loads
+};
+
+struct DequantArgs {
+    const uint8_t* packed;
+    const float* zmin;
+    const float* scale;
+    const uint8_t* bits;
+    const int64_t* off;
+    int64_t N, D, ng;
+    void* out;
+    int out_dt;
+    bool fast;
+};
+
+struct StatsArgs {
+    const void* x;
+    int dt;
+    int64_t N, D, ng, nch;
+    float* gmin;
+    float* gmax;
+    double* sens;
+    double* T;  // workspace [N * nch]
+    bool fast;
+};
+
+struct AllocArgs {
+    const double* sens;
+    const double* gscale;
+    int64_t N;
+    int64_t need;  // N * L[0] - budget (bits to free); <= 0 => all at L[0]
+    int m;         // number of levels
+    int L[8];      // levels, descending
+    double slope[8];
+    int freed[8];
+    int64_t unit;  // bytes per bit of width per sample: ng * G / 8
+    uint8_t* bits;
+    int64_t* off;
+};
+
+cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
+cudaError_t launch_dequantize(const DequantArgs& a, cudaStream_t s);
+cudaError_t launch_group_stats(const StatsArgs& a, cudaStream_t s);
+cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s);
+cudaError_t launch_uniform_bits(int64_t N, int b, int64_t unit, uint8_t* bits, int64_t* off,
+                                cudaStream_t s);
+
+// persistent-grid sizing: min(work, SMs * resident blocks per SM)
+int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks);
+
+}  // namespace actnn

@@ -1,0 +1,147 @@
+// stats.cu -- K1 group_stats + K1b sens_reduce: pass 1 of the mixed-precision
+// path.  Per group the canonical min Z and max M; per sample the
+// range norm S_n = ||R_n||^2 (the ||R_n||^2 factor of w_n in Eq. 7),
+// summed in ACTNN-Q v1's canonical order O11 so that the allocator sees the
+// same fp64 values as the oracle:
+//   K1: a CTA (8 warps) owns one chunk of 32 groups of one sample; warp w
+//       reduces groups 4w..4w+3 (one 256-bit load per lane per group, 4 groups
+//       in flight), the 32 (Z, M) pairs meet in shared memory, and warp 0
+//       writes them coalesced and runs the fp64 xor butterfly over
+//       v_l = R_l^2 (lane l = group l; zero past the sample's last group):
+//       T_{n,c} = v_0 after v_l <- v_l + v_{l^o}, o = 16, 8, 4, 2, 1.
+//   K1b: S_n = ((0 + T_{n,0}) + T_{n,1}) + ... in chunk order.
+#include "device.cuh"
+#include "launch.h"
+
+namespace actnn {
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kU = 4;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct SParams {
+    const void* x;
+    int64_t N, D, ng, nch;
+    float* gmin;
+    float* gmax;
+    double* T;
+};
+
+template <typename T, bool kFast>
+__global__ void __launch_bounds__(kBlock) group_stats_kernel(SParams p) {
+    __shared__ float sZ[kChunk], sM[kChunk];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const T* __restrict__ x = static_cast<const T*>(p.x);
+    const int64_t tiles = p.N * p.nch;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t n = t / p.nch;
+        const int64_t c = t - n * p.nch;
+        const int64_t g0 = c * kChunk;
+        const int gcount = (int)min((int64_t)kChunk, p.ng - g0);
+        const int gw = w * kU;  // this warp's first group within the chunk
+        float myMn = 0.0f, myMx = 0.0f;
+        if (kFast) {
+            float v[kU][8];
+            const T* src = x + n * p.D + (g0 + gw) * kG + lane * 8;
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                if (gw + u < gcount) load8(src + u * kG, v[u]);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (gw + u < gcount) {
+                    float mn = v[u][0], mx = v[u][0];
+#pragma unroll
+                    for (int j = 1; j < 8; ++j) {
+                        mn = fminf(mn, v[u][j]);
+                        mx = fmaxf(mx, v[u][j]);
+                    }
+                    mn = warp_min(mn);
+                    mx = warp_max(mx);
+                    if (lane == u) {
+                        myMn = mn;
+                        myMx = mx;
+                    }
+                }
+            }
+        } else {
+            for (int u = 0; u < kU; ++u) {
+                if (gw + u < gcount) {
+                    const int64_t i = g0 + gw + u;
+                    const int len = (int)min((int64_t)kG, p.D - i * kG);
+                    const T* src = x + n * p.D + i * kG;
+                    float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+                    for (int j = 0; j < 8; ++j) {
+                        const int idx = lane * 8 + j;
+                        if (idx < len) {
+                            const float h = load1(src + idx);
+                            mn = fminf(mn, h);
+                            mx = fmaxf(mx, h);
+                        }
+                    }
+                    mn = warp_min(mn);
+                    mx = warp_max(mx);
+                    if (lane == u) {
+                        myMn = mn;
+                        myMx = mx;
+                    }
+                }
+            }
+        }
+        if (lane < kU && gw + lane < gcount) {
+            sZ[gw + lane] = __fadd_rn(myMn, 0.0f);  // canonical +0 (DESIGN reading 17)
+            sM[gw + lane] = __fadd_rn(myMx, 0.0f);
+        }
+        __syncthreads();
+        if (w == 0) {
+            double v = 0.0;
+            if (lane < gcount) {
+                const float Z = sZ[lane], M = sM[lane];
+                p.gmin[n * p.ng + g0 + lane] = Z;
+                p.gmax[n * p.ng + g0 + lane] = M;
+                const float R = __fsub_rn(M, Z);
+                v = __dmul_rn((double)R, (double)R);  // exact: 24b x 24b < 53b
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
+            if (lane == 0) p.T[t] = v;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void sens_reduce_kernel(const double* __restrict__ T, int64_t N, int64_t nch,
+                                   double* __restrict__ sens) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    double s = 0.0;
+    for (int64_t c = 0; c < nch; ++c) s = __dadd_rn(s, T[n * nch + c]);
+    sens[n] = s;
+}
+
+template <typename T>
+cudaError_t run(const StatsArgs& a, cudaStream_t s) {
+    SParams p{a.x, a.N, a.D, a.ng, a.nch, a.gmin, a.gmax, a.T};
+    const int64_t tiles = a.N * a.nch;
+    if (a.fast) {
+        const int grid = grid_for((const void*)group_stats_kernel<T, true>, kBlock, 0, tiles);
+        group_stats_kernel<T, true><<<grid, kBlock, 0, s>>>(p);
+    } else {
+        const int grid = grid_for((const void*)group_stats_kernel<T, false>, kBlock, 0, tiles);
+        group_stats_kernel<T, false><<<grid, kBlock, 0, s>>>(p);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int rb = 128;
+    sens_reduce_kernel<<<(unsigned)((a.N + rb - 1) / rb), rb, 0, s>>>(a.T, a.N, a.nch, a.sens);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_group_stats(const StatsArgs& a, cudaStream_t s) {
+    return a.dt == 0 ? run<float>(a, s) : run<uint16_t>(a, s);
+}
+
+}  // namespace actnn

@@ -1,0 +1,147 @@
+"""Preallocated per-step executor for a whole activation set.
+
+A training step compresses every saved activation of the network in the
+forward pass and decompresses it in the backward pass (Fig. 2).
+``ActivationSetPlan`` owns all per-layer buffers, prebuilds the ctypes
+argument tuples of every C-ABI call, and issues the calls on the current
+stream with no per-call allocation, so the CPU stays ahead of the GPU even for
+the small layers.  Mixed precision (L2.5) runs per layer
+  actnn_group_stats -> [all-gather of S over the ranks, k > 1]
+  -> actnn_allocate_bits -> actnn_quantize (with the stats);
+uniform precision (L2) runs actnn_quantize single-pass with fixed widths.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import torch
+
+from . import _lib
+from .api import BF16, F32, G, LEVELS_POW2, OP_GROUP_STATS, ceil_div
+
+_P = ctypes.c_void_p
+
+
+def _p(t: torch.Tensor, offset_elems: int = 0) -> ctypes.c_void_p:
+    return _P(t.data_ptr() + offset_elems * t.element_size())
+
+
+@dataclass
+class Layer:
+    x: torch.Tensor
+    N: int
+    D: int
+    ng: int
+    dt: int
+    seed: int
+    budget: int
+    gmin: torch.Tensor = None
+    gmax: torch.Tensor = None
+    S: torch.Tensor = None          # fp64 [N_total] (global vector)
+    S_loc: torch.Tensor = None      # fp64 [N] this rank's slice (a view of S when k = 1)
+    ws: torch.Tensor = None
+    bits: torch.Tensor = None       # u8 [N_total]
+    off: torch.Tensor = None        # i64 [N_total + 1]
+    packed: torch.Tensor = None
+    zmin: torch.Tensor = None
+    scale: torch.Tensor = None
+    args: dict = field(default_factory=dict)
+
+
+class ActivationSetPlan:
+    def __init__(self, xs: Sequence[torch.Tensor], seeds: Sequence[int],
+                 avg_bits: Optional[float] = None, bits: Optional[int] = None,
+                 level_mask: int = LEVELS_POW2, n_total: Optional[int] = None,
+                 sample_base: int = 0,
+                 gather: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None):
+        if (avg_bits is None) == (bits is None):
+            raise ValueError("give exactly one of avg_bits / bits")
+        self.lib = _lib.load()
+        self.mixed = avg_bits is not None
+        # k > 1: gather(S_global, S_local) fills S_global[N_total] with every
+        # rank's S_n (an all-gather over NCCL: the exchange step, equivalent
+        # to the all-reduce of zero-padded vectors and exact)
+        self.gather = gather
+        self.layers: List[Layer] = []
+        self.sample_base = sample_base
+        lib = self.lib
+        for x, seed in zip(xs, seeds):
+            x2 = x.reshape(x.shape[0], -1)
+            N, D = x2.shape
+            nt = n_total if n_total is not None else N
+            ng = ceil_div(D, G)
+            dev = x2.device
+            dt = F32 if x2.dtype == torch.float32 else BF16
+            budget = int(avg_bits * nt) if self.mixed else bits * nt
+            L = Layer(x2, N, D, ng, dt, seed, budget)
+            unit = ng * G // 8
+            # Sum_n b_n <= budget globally, so this rank's slice needs at most
+            # min(8 N, budget) * unit bytes.
+            cap = min(8 * N, budget) * unit
+            L.packed = torch.empty(max(cap, 16), dtype=torch.uint8, device=dev)
+            L.zmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
+            L.scale = torch.empty(N * ng, dtype=torch.float32, device=dev)
+            L.bits = torch.empty(nt, dtype=torch.uint8, device=dev)
+            L.off = torch.empty(nt + 1, dtype=torch.int64, device=dev)
+            lo = sample_base if nt != N else 0
+            bits_p, off_p = _p(L.bits, lo), _p(L.off, lo)
+            if self.mixed:
+                L.gmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
+                L.gmax = torch.empty(N * ng, dtype=torch.float32, device=dev)
+                L.S = torch.zeros(nt, dtype=torch.float64, device=dev)
+                L.S_loc = (torch.zeros(N, dtype=torch.float64, device=dev) if nt != N
+                           else L.S)
+                wsb = int(lib.actnn_workspace_bytes(OP_GROUP_STATS, N, D, G))
+                L.ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+                L.args["stats"] = (_p(x2), dt, N, D, G, _p(L.gmin), _p(L.gmax), _p(L.S_loc),
+                                   _p(L.ws), L.ws.numel())
+                L.args["alloc"] = (_p(L.S), None, nt, budget, level_mask, D, G, _p(L.bits),
+                                   _p(L.off), None, 0)
+                L.args["quant"] = (_p(x2), dt, N, D, G, bits_p, off_p, ctypes.c_uint64(seed),
+                                   sample_base, _p(L.gmin), _p(L.gmax), _p(L.packed),
+                                   _p(L.zmin), _p(L.scale))
+            else:
+                # L2: fixed widths, written once (not part of a step)
+                _lib.check(lib.actnn_uniform_bits(nt, D, G, bits, _p(L.bits), _p(L.off),
+                                                  _P(torch.cuda.current_stream(dev).cuda_stream)))
+                L.args["quant"] = (_p(x2), dt, N, D, G, bits_p, off_p, ctypes.c_uint64(seed),
+                                   sample_base, None, None, _p(L.packed), _p(L.zmin),
+                                   _p(L.scale))
+            L.args["dequant"] = (_p(L.packed), _p(L.zmin), _p(L.scale), bits_p, off_p, N, D, G)
+            self.layers.append(L)
+
+    # launches per step: stats (2 kernels) + allocate + quantize + dequantize
+    def launches_per_step(self) -> int:
+        return len(self.layers) * (5 if self.mixed else 2)
+
+    def compress_layer(self, i: int, stream: ctypes.c_void_p, ev=None):
+        lib, L = self.lib, self.layers[i]
+        if self.mixed:
+            if ev is not None:
+                ev[0].record()
+            _lib.check(lib.actnn_group_stats(*L.args["stats"], stream))
+            if ev is not None:
+                ev[1].record()
+            if self.gather is not None:
+                self.gather(L.S, L.S_loc)
+            _lib.check(lib.actnn_allocate_bits(*L.args["alloc"], stream))
+        if ev is not None:
+            ev[2].record()
+        _lib.check(lib.actnn_quantize(*L.args["quant"], stream))
+        if ev is not None:
+            ev[3].record()
+
+    def decompress_layer(self, i: int, out: torch.Tensor, out_dt: int, stream, ev=None):
+        L = self.layers[i]
+        if ev is not None:
+            ev[0].record()
+        _lib.check(self.lib.actnn_dequantize(*L.args["dequant"], _p(out), out_dt, stream))
+        if ev is not None:
+            ev[1].record()
+
+    def bits_host(self):
+        lo = self.sample_base
+        return [L.bits[lo:lo + L.N].cpu() if L.bits.numel() != L.N else L.bits.cpu()
+                for L in self.layers]

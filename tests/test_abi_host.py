@@ -1,0 +1,110 @@
+"""CPU-side checks of the C ABI (no GPU needed): the library loads, exports
+every symbol include/actnn.h declares, and its host-side argument validation
+returns the documented status without launching anything."""
+import ctypes
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2104_14129_b200 import _lib
+
+OK, INVALID, UNSUPPORTED, BUDGET = 0, -1, -2, -3
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return _lib.load()
+
+
+def test_exports_every_header_symbol(lib):
+    names = _lib.header_symbols()
+    assert len(names) == 9
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.SIGNATURES)
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert set(names) <= exported
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_abi_version_and_sizes(lib):
+    assert lib.actnn_abi_version() == 1
+    assert lib.actnn_workspace_bytes(0, 4, 1024, 256) == 4 * 1 * 8
+    assert lib.actnn_workspace_bytes(0, 2, 256 * 33, 256) == 2 * 2 * 8
+    assert lib.actnn_workspace_bytes(1, 4, 1024, 256) == 0
+    assert lib.actnn_packed_bytes(4, 1024, 256, None) == 4 * 4 * 256
+    bits = np.array([1, 2, 4, 8], np.uint8)
+    p = bits.ctypes.data_as(ctypes.c_void_p)
+    assert lib.actnn_packed_bytes(4, 1000, 256, p) == 15 * 4 * 32
+    bad = np.array([0, 9], np.uint8)
+    assert lib.actnn_packed_bytes(2, 256, 256, bad.ctypes.data_as(ctypes.c_void_p)) == -1
+
+
+def _msg(lib):
+    return lib.actnn_last_error().decode()
+
+
+def test_quantize_host_validation(lib):
+    d = ctypes.c_void_p(0x1000)  # never dereferenced: validation fails first
+    q = lib.actnn_quantize
+    assert q(None, 0, 4, 1024, 256, d, d, 1, 0, None, None, d, d, d, None) == INVALID
+    assert "null" in _msg(lib)
+    assert q(d, 0, 4, 1024, 128, d, d, 1, 0, None, None, d, d, d, None) == UNSUPPORTED
+    assert q(d, 0, -1, 1024, 256, d, d, 1, 0, None, None, d, d, d, None) == INVALID
+    assert q(d, 7, 4, 1024, 256, d, d, 1, 0, None, None, d, d, d, None) == INVALID
+    assert q(d, 0, 4, 1024, 256, d, d, 1, 0, d, None, d, d, d, None) == INVALID
+    assert q(d, 0, 4, 1024, 256, d, d, 1, -5, None, None, d, d, d, None) == INVALID
+    unal = ctypes.c_void_p(0x1008)
+    assert q(d, 0, 4, 1024, 256, d, d, 1, 0, None, None, unal, d, d, None) == UNSUPPORTED
+    assert q(ctypes.c_void_p(0x1002), 0, 4, 1024, 256, d, d, 1, 0, None, None, d, d, d,
+             None) == INVALID
+    # empty problems are valid no-ops
+    assert q(None, 0, 0, 1024, 256, None, None, 1, 0, None, None, None, None, None, None) == OK
+    assert q(None, 0, 4, 0, 256, None, None, 1, 0, None, None, None, None, None, None) == OK
+
+
+def test_dequantize_and_stats_host_validation(lib):
+    d = ctypes.c_void_p(0x1000)
+    dq = lib.actnn_dequantize
+    assert dq(None, d, d, d, d, 4, 1024, 256, d, 0, None) == INVALID
+    assert dq(d, d, d, d, d, 4, 1024, 512, d, 0, None) == UNSUPPORTED
+    assert dq(d, d, d, d, d, 4, 1024, 256, d, 3, None) == INVALID
+    assert dq(None, None, None, None, None, 0, 1024, 256, None, 0, None) == OK
+    gs = lib.actnn_group_stats
+    assert gs(d, 0, 4, 1024, 256, d, d, d, d, 0, None) == INVALID   # workspace too small
+    assert "workspace" in _msg(lib)
+    assert gs(d, 0, 4, 1024, 256, d, None, d, d, 64, None) == INVALID
+    assert gs(None, 0, 0, 1024, 256, None, None, None, None, 0, None) == OK
+
+
+def test_allocate_host_validation(lib):
+    d = ctypes.c_void_p(0x1000)
+    al = lib.actnn_allocate_bits
+    POW2 = 0x116
+    assert al(d, None, 10, 9, POW2, 1024, 256, d, d, None, 0, None) == BUDGET
+    assert "infeasible" in _msg(lib)
+    assert al(d, None, 10, 40, 0x201, 1024, 256, d, d, None, 0, None) == INVALID
+    assert al(d, None, 10, 40, 0, 1024, 256, d, d, None, 0, None) == INVALID
+    assert al(None, None, 10, 40, POW2, 1024, 256, d, d, None, 0, None) == INVALID
+    assert al(d, None, 10, 40, POW2, 1024, 100, d, d, None, 0, None) == UNSUPPORTED
+    # unit-step mask: infeasible below N * 1
+    assert al(d, None, 10, 9, 0x1FE, 1024, 256, d, d, None, 0, None) == BUDGET
+    ub = lib.actnn_uniform_bits
+    assert ub(4, 1024, 256, 0, d, d, None) == INVALID
+    assert ub(4, 1024, 256, 9, d, d, None) == INVALID
+
+
+def test_python_binding_refuses_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    import paper_2104_14129_b200 as A
+    with pytest.raises(A.ActnnError):
+        A.quantize(torch.zeros(4, 1024), torch.zeros(4, dtype=torch.uint8),
+                   torch.zeros(5, dtype=torch.int64), 0)
