@@ -158,11 +158,19 @@ def cpu_sample(wl, acts, args, target_s, seed_of, torch):
                 out.append(x.numpy())
         return out
 
-    xs1 = host_inputs(1)
-    t1 = run(1, xs1)
-    n_s = max(1, min(wl.N, int(target_s / max(t1, 1e-3))))
-    xs = host_inputs(n_s) if n_s > 1 else xs1
-    t = run(n_s, xs)
+    # calibrate: double the sample until one run takes >= target/4, then scale
+    n_s, t = 1, 0.0
+    while True:
+        xs = host_inputs(n_s)
+        t = run(n_s, xs)
+        if t >= target_s / 4 or n_s >= wl.N:
+            break
+        n_s = min(wl.N, 2 * n_s)
+    n_new = max(1, min(wl.N, int(n_s * target_s / max(t, 1e-3))))
+    if n_new > n_s:
+        n_s = n_new
+        xs = host_inputs(n_s)
+        t = run(n_s, xs)
     E = n_s * sum(a.D for a in acts)
     s_in = 4 if wl.dtype == "f32" else 2
     return {"value": E * s_in / t / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",

@@ -59,7 +59,10 @@ def _as_2d(x: torch.Tensor) -> torch.Tensor:
     if not x.is_contiguous():
         raise ActnnError(-1, "actnn needs a contiguous [N, ...] activation")
     N = x.shape[0] if x.dim() > 0 else 1
-    return x.reshape(N, -1)
+    D = 1
+    for s in x.shape[1:]:
+        D *= s
+    return x.reshape(N, D)
 
 
 def ceil_div(a: int, b: int) -> int:
