@@ -81,7 +81,10 @@ int64_t actnn_packed_bytes(int64_t N, int64_t D, int32_t G, const uint8_t* bits_
  * w_n up to the per-sample gradient factor of Eq. 7.
  *   x        [N, D] activations of dtype dt
  *   gmin/gmax [N*ng] fp32 outputs;  sens [N] fp64 output
- *   ws       >= actnn_workspace_bytes(ACTNN_OP_GROUP_STATS, N, D, G) bytes, 8B-aligned */
+ *   ws       >= actnn_workspace_bytes(ACTNN_OP_GROUP_STATS, N, D, G) bytes, 8B-aligned,
+ *            ZERO-FILLED before its first use (its last 8 bytes hold a completion
+ *            ticket that every call leaves at zero again); one workspace per
+ *            stream: concurrent calls must not share it.  One kernel launch. */
 actnn_status_t actnn_group_stats(const void* x, actnn_dtype_t dt, int64_t N, int64_t D, int32_t G,
                                  float* gmin, float* gmax, double* sens, void* ws,
                                  size_t ws_bytes, void* stream);

@@ -125,7 +125,7 @@ def group_stats(x: torch.Tensor, sens_out: Optional[torch.Tensor] = None):
     sens = sens_out if sens_out is not None else torch.empty(N, dtype=torch.float64, device=dev)
     lib = _lib.load()
     wsb = int(lib.actnn_workspace_bytes(OP_GROUP_STATS, N, D, G))
-    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(max(wsb, 8), dtype=torch.uint8, device=dev)
     _lib.check(lib.actnn_group_stats(_ptr(x2), _dtype_code(x2.dtype), N, D, G, _ptr(gmin),
                                      _ptr(gmax), _ptr(sens), _ptr(ws), ws.numel(), _stream(dev)))
     return gmin, gmax, sens

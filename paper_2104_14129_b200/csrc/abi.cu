@@ -110,7 +110,7 @@ int actnn_abi_version(void) { return ACTNN_ABI_VERSION; }
 
 size_t actnn_workspace_bytes(int op, int64_t N, int64_t D, int32_t G) {
     if (N <= 0 || D <= 0 || G <= 0) return 0;
-    if (op == ACTNN_OP_GROUP_STATS) return (size_t)(N * ceil_div(ceil_div(D, G), 32)) * 8;
+    if (op == ACTNN_OP_GROUP_STATS) return (size_t)(N * ceil_div(ceil_div(D, G), 32)) * 8 + 8;
     return 0;
 }
 

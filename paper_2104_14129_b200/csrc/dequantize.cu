@@ -1,9 +1,13 @@
 // dequantize.cu -- K4: unpacker + dequantiser ("During
 // back-propagation, the activation is dequantized as h_hat = u_hat R/B + Z"),
-// ACTNN-Q v1 step O10.  Mirrors K3's layout: a warp's unit is 4 consecutive
-// groups of one sample; lane l reads the b bytes holding its 8 codes and
-// writes its 8 consecutive outputs with one 256-bit (fp32) or 128-bit (bf16)
-// store, so each warp store covers whole 32 B sectors.  The per-group (Z,
+// ACTNN-Q v1 step O10.  Mirrors K3: a warp's unit is 4 consecutive groups of
+// one sample; the unit's packed bytes (contiguous: 4 x 32 b bytes) arrive by
+// cp.async.bulk in a per-warp ring of S shared-memory stages (lane 0 keeps S
+// units in flight); lane l reads the b bytes holding its 8 codes from shared
+// memory and writes its 8 consecutive outputs with one 256-bit (fp32) or
+// 128-bit (bf16) store, so each warp store covers whole 32 B sectors.
+// (float)code uses the exact 2^23 magic; the dequantisation is one
+// __ffma2_rn per element pair (single rounding, O10).  The per-group (Z,
 // scale) pairs are loaded lane-parallel and broadcast by shuffles.
 #include "device.cuh"
 #include "launch.h"
@@ -12,8 +16,14 @@ namespace actnn {
 namespace {
 
 constexpr int kU = 4;
-constexpr int kBlock = 256;
+constexpr int kWarps = 8;
+constexpr int kBlock = kWarps * 32;
+constexpr int kS = 4;                    // stages per warp
+constexpr int kStage = kU * 32 * 8;      // bytes: 4 groups at the widest (b = 8)
+constexpr int kNCap = 2048;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr size_t kSmem = (size_t)kWarps * kS * kStage + (size_t)kWarps * kS * 8 + kNCap +
+                         4 * (kNCap + 1);
 
 struct DParams {
     const uint8_t* packed;
@@ -21,107 +31,196 @@ struct DParams {
     const float* scale;
     const uint8_t* bits;
     const int64_t* off;
-    int64_t N, D, ng, nb, units;
-    uint64_t nb_magic;
+    uint32_t N, D, ng, nb;
+    uint32_t step_n, step_j;  // unit stride of a warp: nwarps = step_n * nb + step_j
     void* out;
 };
 
-__device__ __forceinline__ int64_t div_nb(int64_t u, int64_t nb, uint64_t magic) {
-    if (nb == 1) return u;
-    if ((uint64_t)u >> 32) return u / nb;
-    return (int64_t)__umul64hi((uint64_t)u, magic);
-}
+struct GDParams {  // generic kernel
+    const uint8_t* packed;
+    const float* zmin;
+    const float* scale;
+    const uint8_t* bits;
+    const int64_t* off;
+    int64_t N, D, ng;
+    void* out;
+};
 
-// The b bytes of lane `lane` in a group segment, as a little-endian integer.
+// The b bytes of a lane in a staged group segment, as a little-endian integer.
 template <int b>
-__device__ __forceinline__ uint64_t load_payload(const uint8_t* seg, int lane) {
-    // volatile asm keeps each width's loads inside its own switch arm (ptxas
-    // otherwise hoists all arms' loads and doubles the register footprint)
+__device__ __forceinline__ uint64_t stage_payload(const uint8_t* seg, int lane) {
     if constexpr (b == 8) {
-        uint32_t lo, hi;
-        asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "l"(seg + lane * 8));
-        return (uint64_t)lo | ((uint64_t)hi << 32);
+        return reinterpret_cast<const uint64_t*>(seg)[lane];
     } else if constexpr (b == 4) {
-        uint32_t v;
-        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(seg + lane * 4));
-        return v;
+        return reinterpret_cast<const uint32_t*>(seg)[lane];
     } else if constexpr (b == 2) {
-        uint16_t v;
-        asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(seg + lane * 2));
-        return v;
+        return reinterpret_cast<const uint16_t*>(seg)[lane];
     } else if constexpr (b == 1) {
-        uint32_t v;
-        asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(seg + lane));
-        return v;
+        return seg[lane];
     } else {
         uint64_t p = 0;
 #pragma unroll
-        for (int t = 0; t < b; ++t) {
-            uint32_t v;
-            asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(seg + lane * b + t));
-            p |= (uint64_t)v << (8 * t);
-        }
+        for (int t = 0; t < b; ++t) p |= (uint64_t)seg[lane * b + t] << (8 * t);
         return p;
     }
 }
 
-template <typename TO, int b>
-__device__ __forceinline__ void dequant_unit(const uint8_t* seg, int gcount, float myZ,
+// Exact float(code) as the bit pattern 0x4B000000 | code (= 2^23 + code).
+template <int b>
+__device__ __forceinline__ uint32_t magic_code(uint64_t pay, int j) {
+    if constexpr (b == 8) {
+        const uint32_t word = j < 4 ? (uint32_t)pay : (uint32_t)(pay >> 32);
+        return __byte_perm(word, 0x4B000000u, 0x7540u | (uint32_t)(j & 3));
+    } else {
+        return (uint32_t)((pay >> (b * j)) & ((1u << b) - 1u)) | 0x4B000000u;
+    }
+}
+
+template <typename TO, int b, bool kFullUnit>
+__device__ __forceinline__ void dequant_unit(const uint8_t* st, int gcount, float myZ,
                                              float mySc, TO* dst, int lane) {
     uint64_t pay[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-        if (u < gcount) pay[u] = load_payload<b>(seg + u * 32 * b, lane);
-    constexpr uint32_t mask = (1u << b) - 1u;
+        if (kFullUnit || u < gcount) pay[u] = stage_payload<b>(st + u * 32 * b, lane);
+    const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-        if (u < gcount) {
+        if (kFullUnit || u < gcount) {
             const float Z = __shfl_sync(kFull, myZ, u);
             const float s = __shfl_sync(kFull, mySc, u);
+            const float2 zz = make_float2(Z, Z), ss = make_float2(s, s);
             float o[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) o[j] = dequant1((uint32_t)(pay[u] >> (b * j)) & mask, s, Z);
+            for (int p = 0; p < 4; ++p) {
+                float2 c = make_float2(__uint_as_float(magic_code<b>(pay[u], 2 * p)),
+                                       __uint_as_float(magic_code<b>(pay[u], 2 * p + 1)));
+                c = __fadd2_rn(c, m23);          // exact: (float)code
+                c = __ffma2_rn(c, ss, zz);       // code * scale + Z, one rounding
+                o[2 * p] = c.x;
+                o[2 * p + 1] = c.y;
+            }
             store8(dst + u * kG + lane * 8, o);
         }
     }
 }
 
+template <typename TO, int b>
+__device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount, float myZ,
+                                                 float mySc, TO* dst, int lane) {
+    if (gcount == kU)
+        dequant_unit<TO, b, true>(st, gcount, myZ, mySc, dst, lane);
+    else
+        dequant_unit<TO, b, false>(st, gcount, myZ, mySc, dst, lane);
+}
+
 template <typename TO>
-__global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(DParams p) {
+__global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid_constant__ DParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    TO* __restrict__ out = static_cast<TO*>(p.out);
+    const int w = threadIdx.x >> 5;
+    uint8_t* ring = smem + (size_t)w * kS * kStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kS * kStage) + w * kS;
+    uint8_t* s_bits = smem + (size_t)kWarps * kS * kStage + (size_t)kWarps * kS * 8;
+    uint32_t* s_off = reinterpret_cast<uint32_t*>(s_bits + kNCap);
+
+    const bool cached = p.N <= (uint32_t)kNCap;
     const int64_t off0 = p.off[0];
-    for (int64_t u = warp; u < p.units; u += nwarps) {
-        const int64_t n = div_nb(u, p.nb, p.nb_magic);
-        const int64_t gi = (u - n * p.nb) * kU;
-        const int gcount = (int)min((int64_t)kU, p.ng - gi);
-        const int b = p.bits[n];
-        const uint8_t* seg = p.packed + (p.off[n] - off0) + gi * 32 * b;
-        const int64_t g = n * p.ng + gi;
-        TO* dst = out + n * p.D + gi * kG;
-        float myZ = 0.0f, mySc = 0.0f;  // lane u holds group u's (Z, scale)
-        if (lane < gcount) {
-            myZ = __ldg(p.zmin + g + lane);
-            mySc = __ldg(p.scale + g + lane);
+    if (cached) {
+        for (uint32_t i = threadIdx.x; i < p.N; i += kBlock) {
+            s_bits[i] = p.bits[i];
+            s_off[i] = (uint32_t)((p.off[i] - off0) >> 5);
         }
-        // warp-uniform dispatch on the sample's width (an if-chain: a switch
-        // becomes an indirect branch that ptxas allocates registers across)
-        if (b == 2) dequant_unit<TO, 2>(seg, gcount, myZ, mySc, dst, lane);
-        else if (b == 1) dequant_unit<TO, 1>(seg, gcount, myZ, mySc, dst, lane);
-        else if (b == 4) dequant_unit<TO, 4>(seg, gcount, myZ, mySc, dst, lane);
-        else if (b == 8) dequant_unit<TO, 8>(seg, gcount, myZ, mySc, dst, lane);
-        else if (b == 3) dequant_unit<TO, 3>(seg, gcount, myZ, mySc, dst, lane);
-        else if (b == 5) dequant_unit<TO, 5>(seg, gcount, myZ, mySc, dst, lane);
-        else if (b == 6) dequant_unit<TO, 6>(seg, gcount, myZ, mySc, dst, lane);
-        else if (b == 7) dequant_unit<TO, 7>(seg, gcount, myZ, mySc, dst, lane);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kS; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint32_t gw = blockIdx.x * kWarps + w;
+    TO* __restrict__ out = static_cast<TO*>(p.out);
+    auto advance = [&](uint32_t& n, uint32_t& j) {
+        n += p.step_n;
+        j += p.step_j;
+        if (j >= p.nb) {
+            j -= p.nb;
+            ++n;
+        }
+    };
+    auto gcount_of = [&](uint32_t j) { return (int)min((uint32_t)kU, p.ng - j * kU); };
+    auto width = [&](uint32_t n) { return cached ? (int)s_bits[n] : (int)p.bits[n]; };
+    auto seg_of = [&](uint32_t n, uint32_t j, int b) {
+        const int64_t sofs = cached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
+        return p.packed + sofs + (uint64_t)j * (kU * 32) * b;
+    };
+    // lane 0 issues the bulk copy of unit (pn, pj) into stage s
+    auto issue = [&](uint32_t pn, uint32_t pj, int s) {
+        int b = width(pn);
+        if (b < 1 || b > 8) b = 1;  // outside the contract; keep the ring's phases consistent
+        const uint32_t bytes = (uint32_t)(gcount_of(pj) * 32 * b);
+        mbar_expect_tx(&bars[s], bytes);
+        bulk_g2s(ring + s * kStage, seg_of(pn, pj, b), bytes, &bars[s]);
+    };
+
+    uint32_t pn = gw / p.nb, pj = gw % p.nb;
+    uint32_t n = pn, j = pj;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kS; ++s) {
+            if (pn < p.N) issue(pn, pj, s);
+            advance(pn, pj);
+        }
+    }
+    float nZ = 0.0f, nSc = 0.0f;  // lane u: (Z, scale) of group u of the current unit
+    if (n < p.N && lane < gcount_of(j)) {
+        const uint32_t g = n * p.ng + j * kU + lane;
+        nZ = __ldg(p.zmin + g);
+        nSc = __ldg(p.scale + g);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    while (n < p.N) {
+        const int gcount = gcount_of(j);
+        const float myZ = nZ, mySc = nSc;
+        uint32_t nn = n, nj = j;
+        advance(nn, nj);
+        if (nn < p.N && lane < gcount_of(nj)) {  // prefetch the next unit's metadata
+            const uint32_t g2 = nn * p.ng + nj * kU + lane;
+            nZ = __ldg(p.zmin + g2);
+            nSc = __ldg(p.scale + g2);
+        }
+        const int b = width(n);
+        TO* dst = out + (uint64_t)n * p.D + (uint64_t)j * (kU * kG);
+        const uint8_t* st = ring + stage * kStage;
+        mbar_wait(&bars[stage], phase);
+        if (b == 2) dequant_unit_any<TO, 2>(st, gcount, myZ, mySc, dst, lane);
+        else if (b == 1) dequant_unit_any<TO, 1>(st, gcount, myZ, mySc, dst, lane);
+        else if (b == 4) dequant_unit_any<TO, 4>(st, gcount, myZ, mySc, dst, lane);
+        else if (b == 8) dequant_unit_any<TO, 8>(st, gcount, myZ, mySc, dst, lane);
+        else if (b == 3) dequant_unit<TO, 3, false>(st, gcount, myZ, mySc, dst, lane);
+        else if (b == 5) dequant_unit<TO, 5, false>(st, gcount, myZ, mySc, dst, lane);
+        else if (b == 6) dequant_unit<TO, 6, false>(st, gcount, myZ, mySc, dst, lane);
+        else if (b == 7) dequant_unit<TO, 7, false>(st, gcount, myZ, mySc, dst, lane);
+        // the stage's loads were consumed by the stores above: re-arm it
+        __syncwarp();
+        if (lane == 0) {
+            if (pn < p.N) issue(pn, pj, stage);
+            advance(pn, pj);
+        }
+        if (++stage == kS) {
+            stage = 0;
+            phase ^= 1u;
+        }
+        n = nn;
+        j = nj;
     }
 }
 
 // Generic path: ragged last group / unaligned output; one group per warp.
 template <typename TO>
-__global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(DParams p) {
+__global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(const __grid_constant__ GDParams p) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -151,26 +250,35 @@ __global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(DParams p) {
 
 template <typename TO>
 cudaError_t run(const DequantArgs& a, cudaStream_t s) {
-    DParams p;
-    p.packed = a.packed;
-    p.zmin = a.zmin;
-    p.scale = a.scale;
-    p.bits = a.bits;
-    p.off = a.off;
-    p.N = a.N;
-    p.D = a.D;
-    p.ng = a.ng;
-    p.nb = (a.ng + kU - 1) / kU;
-    p.units = a.N * p.nb;
-    p.nb_magic = p.nb > 1 ? (uint64_t)(~0ull / (uint64_t)p.nb) + 1ull : 0ull;
-    p.out = a.out;
-    if (a.fast) {
-        const int grid = grid_for((const void*)dequantize_fast_kernel<TO>, kBlock, 0,
-                                  (p.units + 7) / 8);
-        dequantize_fast_kernel<TO><<<grid, kBlock, 0, s>>>(p);
+    const int64_t nb = (a.ng + kU - 1) / kU;
+    const bool fits = a.N * a.ng < (1ll << 31) && a.D < (1ll << 31);
+    if (a.fast && fits) {
+        DParams p;
+        p.packed = a.packed;
+        p.zmin = a.zmin;
+        p.scale = a.scale;
+        p.bits = a.bits;
+        p.off = a.off;
+        p.N = (uint32_t)a.N;
+        p.D = (uint32_t)a.D;
+        p.ng = (uint32_t)a.ng;
+        p.nb = (uint32_t)nb;
+        p.out = a.out;
+        const void* k = (const void*)dequantize_fast_kernel<TO>;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+            attr = true;
+        }
+        const int grid = grid_for(k, kBlock, kSmem, (a.N * nb + kWarps - 1) / kWarps);
+        const uint32_t nwarps = (uint32_t)grid * kWarps;
+        p.step_n = nwarps / p.nb;
+        p.step_j = nwarps % p.nb;
+        dequantize_fast_kernel<TO><<<grid, kBlock, kSmem, s>>>(p);
     } else {
+        GDParams p{a.packed, a.zmin, a.scale, a.bits, a.off, a.N, a.D, a.ng, a.out};
         const int grid = grid_for((const void*)dequantize_generic_kernel<TO>, kBlock, 0,
-                                  (a.N * a.ng + 7) / 8);
+                                  (a.N * a.ng + kWarps - 1) / kWarps);
         dequantize_generic_kernel<TO><<<grid, kBlock, 0, s>>>(p);
     }
     return cudaGetLastError();

@@ -2,20 +2,29 @@
 // (P:491-503 per-group quantisation, "compress them into bit
 // streams"), ACTNN-Q v1 steps O1-O9.
 //
-// Work decomposition (fast path, D % 256 == 0): a warp's unit is U = 4
-// consecutive groups of one sample (4 KB of fp32 input).  Each lane owns 8
-// consecutive elements of every group: one 256-bit load (fp32) or one 128-bit
-// load (bf16) per group, one Philox4x32-10 call per group (8 x 16 random
-// bits), and b contiguous bytes of the packed group segment.  The U loads are
-// issued before any arithmetic so each warp keeps 4 KB in flight.
-//   - group min/max: 8-element local min/max then a 5-step xor shuffle;
+// Fast path (D % 256 == 0, x 32-byte aligned).  A warp's unit is U = 4
+// consecutive groups of one sample.  Each warp owns a ring of S shared-memory
+// stages fed by cp.async.bulk (TMA, SASS UBLKCP): lane 0 keeps the next units
+// in flight, so HBM latency is covered by shared memory, not registers.
+// Lane l owns elements [8l, 8l+8) of every group: one Philox4x32-10 call per
+// group gives its 8 x 16 random bits, and its codes fill bytes [l b, (l+1) b)
+// of the group's 32 b-byte segment.
+//   - units are walked without division: (n, j) advances by the constant
+//     stride (nwarps / nb, nwarps % nb) with one carry;
+//   - group min/max (uniform single pass only): 8-element local min/max, then a
+//     5-step xor shuffle; in the mixed path (gmin, gmax) come from K1 and are
+//     prefetched one unit ahead;
 //   - per-group constants (two IEEE divisions) are computed lane-parallel, lane
-//     u for group u of the unit, then broadcast with one shuffle each;
-//   - packing: b = 8 / 4 lanes store their 8 / 4 bytes directly (256 / 128 B
-//     per warp); b = 2 / 1 pair / quad lanes with shuffles so every store is a
-//     32-bit word and the warp writes whole 32 B sectors (64 / 32 B per group).
-// Ragged D or unaligned x take the generic kernel (scalar loads, one group per
-// warp iteration); it computes exactly the same bytes.
+//     u for group u of the unit, and broadcast with one shuffle each;
+//   - arithmetic per element pair: one __fadd2_rn (h - Z) and one __ffma2_rn
+//     against 1.5*2^23 (f32x2, sm_100); for b <= 2 both codes are formed in the
+//     two 16-bit halves of one integer (q0 + r0 + ((q1 + r1) << 16), no carry as
+//     q + r < 2^16) and moved to their packed position with one IMAD.HI;
+//   - Philox round keys live in the parameter constant bank (no key registers);
+//   - stores: b = 8 / 4 lanes write 8 / 4 bytes; b = 2 / 1 pair / quad lanes
+//     by shuffles so every store is a word and the warp fills whole sectors.
+// Ragged D, unaligned x or huge tensors take the generic kernel (scalar loads,
+// one group per warp iteration); it produces exactly the same bytes.
 #include "device.cuh"
 #include "launch.h"
 
@@ -23,133 +32,274 @@ namespace actnn {
 namespace {
 
 constexpr int kU = 4;
-constexpr int kBlock = 256;
+constexpr int kWarps = 8;
+constexpr int kBlock = kWarps * 32;
+constexpr int kNCap = 2048;  // samples whose (bits, off) are cached in shared memory
 constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T>
+struct Cfg;
+template <>
+struct Cfg<float> {
+    static constexpr int S = 3;          // stages per warp (4 KB each)
+    static constexpr int MinBlocks = 2;  // CTAs per SM
+};
+template <>
+struct Cfg<uint16_t> {
+    static constexpr int S = 4;  // 2 KB each
+    static constexpr int MinBlocks = 3;
+};
+
+template <typename T>
+__host__ __device__ constexpr int stage_bytes() {
+    return kU * kG * (int)sizeof(T);
+}
+template <typename T>
+__host__ __device__ constexpr size_t smem_bytes() {
+    return (size_t)kWarps * Cfg<T>::S * stage_bytes<T>() + (size_t)kWarps * Cfg<T>::S * 8 + kNCap +
+           4 * (kNCap + 1);
+}
 
 struct QParams {
     const void* x;
-    int64_t N, D, ng, nb, units;
-    uint64_t nb_magic;  // ceil(2^64 / nb) (nb >= 2) for the unit -> sample division
+    uint32_t N, D, ng, nb;      // nb = ceil(ng / U) units per sample
+    uint32_t step_n, step_j;    // unit stride of a warp: nwarps = step_n * nb + step_j
+    uint32_t sample_base;
     const uint8_t* bits;
     const int64_t* off;
-    uint32_t k0, k1;
-    int64_t sample_base;
     const float* gmin;
     const float* gmax;
     uint8_t* packed;
     float* zmin;
     float* scale;
+    RoundKeys rk;
 };
 
-// floor(u / nb) for u < 2^32, nb < 2^32 (one 64-bit mulhi).
-__device__ __forceinline__ int64_t div_nb(int64_t u, int64_t nb, uint64_t magic) {
-    if (nb == 1) return u;
-    if ((uint64_t)u >> 32) return u / nb;
-    return (int64_t)__umul64hi((uint64_t)u, magic);
+struct GParams {  // generic kernel
+    const void* x;
+    int64_t N, D, ng;
+    int64_t sample_base;
+    const uint8_t* bits;
+    const int64_t* off;
+    const float* gmin;
+    const float* gmax;
+    uint8_t* packed;
+    float* zmin;
+    float* scale;
+    RoundKeys rk;
+};
+
+// Codes of a lane's 8 elements for b in {1, 2}, packed LSB-first (O8) into the
+// low 8 b bits.  Pair p = elements (2p, 2p+1) uses Philox word p, whose low
+// and high 16-bit halves are the two draws (O6).  With t = bits of
+// fma(h - Z, inv14, 1.5*2^23) = 0x4B400000 + q (O5):
+//   T = t1 * 2^16 + t0 + (w & 0x3FFF3FFF) - 0x4B400000
+//     = (q0 + r0) + (q1 + r1) * 2^16       (mod 2^32; q + r < 2^16 for b <= 2)
+// so code0 = T[14, 14+b) and code1 = T[30, 30+b) (O7).  Masking those bits
+// and one IMAD.HI by a two-term constant moves code0 to bit s = 2pb and code1
+// to bit s + b of the payload; the cross terms land at bits >= 16 and are
+// masked off at the end.
+template <int b>
+__device__ __forceinline__ uint32_t codes_small(const float v[8], float Z, float inv14,
+                                                const Philox4& o) {
+    const float2 nz = make_float2(-Z, -Z);
+    const float2 iv = make_float2(inv14, inv14);
+    const float2 mg = make_float2(12582912.0f, 12582912.0f);
+    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+    uint32_t acc = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
+        const float2 t = __ffma2_rn(d, iv, mg);
+        uint32_t T = __float_as_uint(t.y) * 65536u + __float_as_uint(t.x);
+        T = T + (w[p] & 0x3FFF3FFFu) - 0x4B400000u;
+        if (b == 2) {
+            acc |= __umulhi(T & 0xC000C000u, (1u << (18 + 4 * p)) + (1u << (4 + 4 * p)));
+        } else {
+            acc |= __umulhi(T & 0x40004000u, (1u << (18 + 2 * p)) + (1u << (3 + 2 * p)));
+        }
+    }
+    return acc & ((1u << (8 * b)) - 1u);
 }
 
-// LSB-first packing of a lane's 8 codes (ACTNN-Q v1 O8): code k of
-// the group sits at stream bits [k b, (k+1) b), so lane l's codes fill bytes
-// [l b, (l+1) b) of the group's 32 b-byte segment.
-template <int b>
-__device__ __forceinline__ void pack_store(uint8_t* seg, const uint32_t code[8], int lane) {
-    if constexpr (b == 8) {
-        const uint32_t lo = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
-        const uint32_t hi = code[4] | (code[5] << 8) | (code[6] << 16) | (code[7] << 24);
-        *reinterpret_cast<uint2*>(seg + lane * 8) = make_uint2(lo, hi);
-    } else if constexpr (b == 4) {
-        uint32_t p = 0;
+// Codes for b >= 3 (q up to 2^22): one code per element (scalar fp32 ops; the
+// f32x2 form of this variant miscompiled in testing).
+__device__ __forceinline__ void codes_wide(const float v[8], float Z, float inv14,
+                                          const Philox4& o, uint32_t code[8]) {
+    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) p |= code[j] << (4 * j);
-        *reinterpret_cast<uint32_t*>(seg + lane * 4) = p;
-    } else if constexpr (b == 2) {
-        uint32_t p = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) p |= code[j] << (2 * j);
-        const uint32_t q = __shfl_down_sync(kFull, p, 1);
-        if (!(lane & 1)) *reinterpret_cast<uint32_t*>(seg + lane * 2) = p | (q << 16);
-    } else if constexpr (b == 1) {
-        uint32_t p = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) p |= code[j] << j;
-        const uint32_t q1 = __shfl_down_sync(kFull, p, 1);
-        const uint32_t q2 = __shfl_down_sync(kFull, p, 2);
-        const uint32_t q3 = __shfl_down_sync(kFull, p, 3);
-        if (!(lane & 3))
-            *reinterpret_cast<uint32_t*>(seg + lane) = p | (q1 << 8) | (q2 << 16) | (q3 << 24);
-    } else {  // b in {3, 5, 6, 7}: b bytes per lane, not word aligned
-        uint64_t p = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) p |= (uint64_t)code[j] << (b * j);
-#pragma unroll
-        for (int t = 0; t < b; ++t) seg[lane * b + t] = (uint8_t)(p >> (8 * t));
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t r = ((j & 1) ? (w[j >> 1] >> 16) : w[j >> 1]) & 0x3FFFu;
+        code[j] = sr_code(v[j], Z, inv14, r);
     }
 }
 
-// One group: Philox draw for the lane's 8-element block, SR codes, pack.
+// One group: Philox draw for the lane's 8-element block, SR codes, pack, store
+// (ACTNN-Q v1 O6-O8).  seg = the group's 32 b-byte segment.
 template <int b>
 __device__ __forceinline__ void quant_group(const float v[8], float Z, float inv14, uint64_t blk,
-                                            uint32_t k0, uint32_t k1, uint8_t* seg, int lane) {
-    const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), k0, k1);
-    uint32_t code[8];
+                                            const RoundKeys& rk, uint8_t* seg, int lane) {
+    const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+    if constexpr (b == 2) {
+        const uint32_t pl = codes_small<2>(v, Z, inv14, o);
+        const uint32_t q = __shfl_down_sync(kFull, pl, 1);
+        if (!(lane & 1)) *reinterpret_cast<uint32_t*>(seg + lane * 2) = pl | (q << 16);
+    } else if constexpr (b == 1) {
+        const uint32_t pl = codes_small<1>(v, Z, inv14, o);
+        const uint32_t q1 = __shfl_down_sync(kFull, pl, 1);
+        const uint32_t q2 = __shfl_down_sync(kFull, pl, 2);
+        const uint32_t q3 = __shfl_down_sync(kFull, pl, 3);
+        if (!(lane & 3))
+            *reinterpret_cast<uint32_t*>(seg + lane) = pl | (q1 << 8) | (q2 << 16) | (q3 << 24);
+    } else {
+        uint32_t code[8];
+        codes_wide(v, Z, inv14, o, code);
+        if constexpr (b == 8) {
+            const uint32_t lo = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
+            const uint32_t hi = code[4] | (code[5] << 8) | (code[6] << 16) | (code[7] << 24);
+            *reinterpret_cast<uint2*>(seg + lane * 8) = make_uint2(lo, hi);
+        } else if constexpr (b == 4) {
+            uint32_t pl = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) code[j] = sr_code(v[j], Z, inv14, rnd14(o, j));
-    pack_store<b>(seg, code, lane);
+            for (int j = 0; j < 8; ++j) pl |= code[j] << (4 * j);
+            *reinterpret_cast<uint32_t*>(seg + lane * 4) = pl;
+        } else {  // b in {3, 5, 6, 7}: b bytes per lane, not word aligned
+            uint64_t pl = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pl |= (uint64_t)code[j] << (b * j);
+#pragma unroll
+            for (int t = 0; t < b; ++t) seg[lane * b + t] = (uint8_t)(pl >> (8 * t));
+        }
+    }
 }
 
-// Width-dependent tail of a unit: lane-parallel group constants (lane u owns
-// group u of the unit), then codes + packing for each group.
-template <int b>
+// Width-dependent part of a unit: lane-parallel constants (lane u owns group
+// u of the unit), then codes + packing of each group.  kFullUnit: gcount == U.
+template <int b, bool kFullUnit>
 __device__ __forceinline__ void quant_unit(const float (&v)[kU][8], int gcount, float myMn,
                                            float myMx, float* zm, float* sc, uint8_t* seg,
-                                           uint64_t blk0, uint32_t k0, uint32_t k1, int lane) {
+                                           uint64_t blk0, const RoundKeys& rk, int lane) {
     const GroupConst cc = group_const(myMn, myMx, b);
-    if (lane < gcount) {
+    if (lane < (kFullUnit ? kU : gcount)) {
         zm[lane] = cc.Z;
         sc[lane] = cc.scale;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-        if (u < gcount) {
+        if (kFullUnit || u < gcount) {
             const float Z = __shfl_sync(kFull, cc.Z, u);
             const float inv = __shfl_sync(kFull, cc.inv14, u);
-            quant_group<b>(v[u], Z, inv, blk0 + (uint64_t)(u * 32 + lane), k0, k1,
-                           seg + u * 32 * b, lane);
+            quant_group<b>(v[u], Z, inv, blk0 + (uint64_t)(u * 32 + lane), rk, seg + u * 32 * b,
+                           lane);
         }
     }
 }
 
+template <int b>
+__device__ __forceinline__ void quant_unit_any(const float (&v)[kU][8], int gcount, float myMn,
+                                               float myMx, float* zm, float* sc, uint8_t* seg,
+                                               uint64_t blk0, const RoundKeys& rk, int lane) {
+    if (gcount == kU)
+        quant_unit<b, true>(v, gcount, myMn, myMx, zm, sc, seg, blk0, rk, lane);
+    else
+        quant_unit<b, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, rk, lane);
+}
+
 template <typename T, bool kStats>
-__global__ void __launch_bounds__(kBlock, 3) quantize_fast_kernel(QParams p) {
+__global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
+    quantize_fast_kernel(const __grid_constant__ QParams p) {
+    constexpr int S = Cfg<T>::S;
+    constexpr int SE = stage_bytes<T>() / (int)sizeof(T);  // elements per stage
+    extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
-    const T* __restrict__ x = static_cast<const T*>(p.x);
+    const int w = threadIdx.x >> 5;
+    T* ring = reinterpret_cast<T*>(smem) + (size_t)w * S * SE;
+    uint64_t* bars =
+        reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * S * stage_bytes<T>()) + w * S;
+    uint8_t* s_bits = smem + (size_t)kWarps * S * stage_bytes<T>() + (size_t)kWarps * S * 8;
+    uint32_t* s_off = reinterpret_cast<uint32_t*>(s_bits + kNCap);
+
+    const bool cached = p.N <= (uint32_t)kNCap;
     const int64_t off0 = p.off[0];
-    for (int64_t u = warp; u < p.units; u += nwarps) {
-        const int64_t n = div_nb(u, p.nb, p.nb_magic);
-        const int64_t gi = (u - n * p.nb) * kU;  // first group of the unit within sample n
-        const int gcount = (int)min((int64_t)kU, p.ng - gi);
-        const int b = p.bits[n];
-        const T* src = x + n * p.D + gi * kG;
-        const int64_t g = n * p.ng + gi;
-        uint8_t* seg = p.packed + (p.off[n] - off0) + gi * 32 * b;
-        const uint64_t blk0 = ((uint64_t)(p.sample_base + n) * (uint64_t)p.D + (uint64_t)(gi * kG)) >> 3;
-        // issue the unit's loads first: 4 groups (4 KB fp32) in flight per warp
+    if (cached) {
+        for (uint32_t i = threadIdx.x; i < p.N; i += kBlock) {
+            s_bits[i] = p.bits[i];
+            s_off[i] = (uint32_t)((p.off[i] - off0) >> 5);  // offsets are multiples of 32 B
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint32_t gw = blockIdx.x * kWarps + w;
+    const T* __restrict__ x = static_cast<const T*>(p.x);
+    auto advance = [&](uint32_t& n, uint32_t& j) {
+        n += p.step_n;
+        j += p.step_j;
+        if (j >= p.nb) {
+            j -= p.nb;
+            ++n;
+        }
+    };
+    auto gcount_of = [&](uint32_t j) { return (int)min((uint32_t)kU, p.ng - j * kU); };
+
+    // producer state (lane 0): the next unit to bulk-copy
+    uint32_t pn = gw / p.nb, pj = gw % p.nb;
+    uint32_t n = pn, j = pj;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (pn < p.N) {
+                const uint32_t bytes = (uint32_t)(gcount_of(pj) * kG * (int)sizeof(T));
+                mbar_expect_tx(&bars[s], bytes);
+                bulk_g2s(ring + s * SE, x + (uint64_t)pn * p.D + (uint64_t)pj * (kU * kG), bytes,
+                         &bars[s]);
+            }
+            advance(pn, pj);
+        }
+    }
+    // mixed path: (gmin, gmax) of the current unit, prefetched one unit ahead
+    float nMn = 0.0f, nMx = 0.0f;
+    if (!kStats && n < p.N && lane < gcount_of(j)) {
+        const uint32_t g = n * p.ng + j * kU + lane;
+        nMn = __ldg(p.gmin + g);
+        nMx = __ldg(p.gmax + g);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    while (n < p.N) {
+        const int gcount = gcount_of(j);
+        const uint32_t gi = j * kU;
+        const uint32_t g = n * p.ng + gi;
+        float myMn = nMn, myMx = nMx;
+        uint32_t nn = n, nj = j;
+        advance(nn, nj);
+        if (!kStats && nn < p.N && lane < gcount_of(nj)) {
+            const uint32_t g2 = nn * p.ng + nj * kU + lane;
+            nMn = __ldg(p.gmin + g2);
+            nMx = __ldg(p.gmax + g2);
+        }
+        const int b = cached ? (int)s_bits[n] : (int)p.bits[n];
+        const int64_t sofs = cached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
+
+        mbar_wait(&bars[stage], phase);
         float v[kU][8];
+        const T* st = ring + stage * SE;
 #pragma unroll
         for (int k = 0; k < kU; ++k)
-            if (k < gcount) load8(src + k * kG + lane * 8, v[k]);
-        float myMn = 0.0f, myMx = 0.0f;
+            if (k < gcount) lds8(st + k * kG + lane * 8, v[k]);
         if constexpr (kStats) {
 #pragma unroll
             for (int k = 0; k < kU; ++k) {
                 if (k < gcount) {
                     float mn = v[k][0], mx = v[k][0];
 #pragma unroll
-                    for (int j = 1; j < 8; ++j) {
-                        mn = fminf(mn, v[k][j]);
-                        mx = fmaxf(mx, v[k][j]);
+                    for (int jj = 1; jj < 8; ++jj) {
+                        mn = fminf(mn, v[k][jj]);
+                        mx = fmaxf(mx, v[k][jj]);
                     }
                     mn = warp_min(mn);
                     mx = warp_max(mx);
@@ -159,34 +309,50 @@ __global__ void __launch_bounds__(kBlock, 3) quantize_fast_kernel(QParams p) {
                     }
                 }
             }
-        } else {
-            if (lane < gcount) {
-                myMn = __ldg(p.gmin + g + lane);
-                myMx = __ldg(p.gmax + g + lane);
-            }
         }
+        uint8_t* seg = p.packed + sofs + (uint64_t)gi * 32 * b;
+        const uint64_t blk0 = (uint64_t)(p.sample_base + n) * (p.D >> 3) + (uint64_t)gi * 32;
         float* zm = p.zmin + g;
         float* sc = p.scale + g;
         switch (b) {
-            case 1: quant_unit<1>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
-            case 2: quant_unit<2>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
-            case 4: quant_unit<4>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
-            case 8: quant_unit<8>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
-            case 3: quant_unit<3>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
-            case 5: quant_unit<5>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
-            case 6: quant_unit<6>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
-            case 7: quant_unit<7>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.k0, p.k1, lane); break;
+            case 1: quant_unit_any<1>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 2: quant_unit_any<2>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 4: quant_unit_any<4>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 8: quant_unit_any<8>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 3: quant_unit<3, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 5: quant_unit<5, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 6: quant_unit<6, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 7: quant_unit<7, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
             default: break;  // invalid width: outside the contract (ACTNN_CHECK=1 reports it)
         }
+        // Every lane's reads of this stage were consumed above; re-arm it with the
+        // unit S ahead.  (In-warp WAR: the generic-proxy loads have completed, so
+        // the async-proxy write cannot overtake them.)
+        __syncwarp();
+        if (lane == 0) {
+            if (pn < p.N) {
+                const uint32_t bytes = (uint32_t)(gcount_of(pj) * kG * (int)sizeof(T));
+                mbar_expect_tx(&bars[stage], bytes);
+                bulk_g2s(ring + stage * SE, x + (uint64_t)pn * p.D + (uint64_t)pj * (kU * kG),
+                         bytes, &bars[stage]);
+            }
+            advance(pn, pj);
+        }
+        if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+        }
+        n = nn;
+        j = nj;
     }
 }
 
 // Generic path: any D (ragged last group), any element alignment.  One group
 // per warp iteration; lane l holds elements [8l, 8l+8) of the group, masked
-// past the group's real length; the Philox block of element e is e >> 3, so
-// a lane needs at most two blocks when D % 8 != 0.
+// past the group's real length; the Philox block of element e is e >> 3, so a
+// lane needs at most two blocks when D % 8 != 0.
 template <typename T, bool kStats>
-__global__ void __launch_bounds__(kBlock) quantize_generic_kernel(QParams p) {
+__global__ void __launch_bounds__(kBlock) quantize_generic_kernel(const __grid_constant__ GParams p) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -203,12 +369,12 @@ __global__ void __launch_bounds__(kBlock) quantize_generic_kernel(QParams p) {
         float v[8];
         float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int idx = lane * 8 + j;
-            v[j] = idx < len ? load1(src + idx) : 0.0f;
+        for (int jj = 0; jj < 8; ++jj) {
+            const int idx = lane * 8 + jj;
+            v[jj] = idx < len ? load1(src + idx) : 0.0f;
             if (idx < len) {
-                mn = fminf(mn, v[j]);
-                mx = fmaxf(mx, v[j]);
+                mn = fminf(mn, v[jj]);
+                mx = fmaxf(mx, v[jj]);
             }
         }
         if (kStats) {
@@ -226,17 +392,18 @@ __global__ void __launch_bounds__(kBlock) quantize_generic_kernel(QParams p) {
         const uint64_t e_first =
             (uint64_t)(p.sample_base + n) * (uint64_t)p.D + (uint64_t)(i * kG + lane * 8);
         const uint64_t blkA = e_first >> 3;
-        const Philox4 oA = philox4x32_10((uint32_t)blkA, (uint32_t)(blkA >> 32), p.k0, p.k1);
+        const Philox4 oA = philox4x32_10((uint32_t)blkA, (uint32_t)(blkA >> 32), p.rk);
         const uint64_t blkB = blkA + 1;
-        const Philox4 oB = philox4x32_10((uint32_t)blkB, (uint32_t)(blkB >> 32), p.k0, p.k1);
+        const Philox4 oB = philox4x32_10((uint32_t)blkB, (uint32_t)(blkB >> 32), p.rk);
         uint64_t pk = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int idx = lane * 8 + j;
-            const uint64_t e = e_first + j;
-            const uint32_t r = ((e >> 3) == blkA) ? rnd14(oA, (int)(e & 7)) : rnd14(oB, (int)(e & 7));
-            const uint32_t code = idx < len ? sr_code(v[j], cc.Z, cc.inv14, r) : 0u;
-            pk |= (uint64_t)code << (b * j);
+        for (int jj = 0; jj < 8; ++jj) {
+            const int idx = lane * 8 + jj;
+            const uint64_t e = e_first + jj;
+            const uint32_t r =
+                ((e >> 3) == blkA) ? rnd14(oA, (int)(e & 7)) : rnd14(oB, (int)(e & 7));
+            const uint32_t code = idx < len ? sr_code(v[jj], cc.Z, cc.inv14, r) : 0u;
+            pk |= (uint64_t)code << (b * jj);
         }
         uint8_t* seg = p.packed + (p.off[n] - off0) + i * 32 * b;
         for (int t = 0; t < b; ++t) seg[lane * b + t] = (uint8_t)(pk >> (8 * t));
@@ -245,31 +412,56 @@ __global__ void __launch_bounds__(kBlock) quantize_generic_kernel(QParams p) {
 
 template <typename T, bool kStats>
 cudaError_t run(const QuantArgs& a, cudaStream_t s) {
-    QParams p;
-    p.x = a.x;
-    p.N = a.N;
-    p.D = a.D;
-    p.ng = a.ng;
-    p.nb = (a.ng + kU - 1) / kU;
-    p.units = a.N * p.nb;
-    p.nb_magic = p.nb > 1 ? (uint64_t)(~0ull / (uint64_t)p.nb) + 1ull : 0ull;
-    p.bits = a.bits;
-    p.off = a.off;
-    p.k0 = (uint32_t)a.seed;
-    p.k1 = (uint32_t)(a.seed >> 32);
-    p.sample_base = a.sample_base;
-    p.gmin = a.gmin;
-    p.gmax = a.gmax;
-    p.packed = a.packed;
-    p.zmin = a.zmin;
-    p.scale = a.scale;
-    if (a.fast) {
+    const int64_t nb = (a.ng + kU - 1) / kU;
+    // fast path: 32-bit unit walk (N * ng, D, sample_base + N < 2^31)
+    const bool fits = a.N * a.ng < (1ll << 31) && a.D < (1ll << 31) &&
+                      a.sample_base + a.N < (1ll << 31);
+    if (a.fast && fits) {
+        QParams p;
+        p.x = a.x;
+        p.N = (uint32_t)a.N;
+        p.D = (uint32_t)a.D;
+        p.ng = (uint32_t)a.ng;
+        p.nb = (uint32_t)nb;
+        p.sample_base = (uint32_t)a.sample_base;
+        p.bits = a.bits;
+        p.off = a.off;
+        p.gmin = a.gmin;
+        p.gmax = a.gmax;
+        p.packed = a.packed;
+        p.zmin = a.zmin;
+        p.scale = a.scale;
+        p.rk = make_round_keys(a.seed);
         const void* k = (const void*)quantize_fast_kernel<T, kStats>;
-        const int grid = grid_for(k, kBlock, 0, (p.units + 7) / 8);
-        quantize_fast_kernel<T, kStats><<<grid, kBlock, 0, s>>>(p);
+        static bool attr = false;  // one-time opt-in above 48 KB of dynamic smem
+        if (!attr) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_bytes<T>());
+            attr = true;
+        }
+        const int64_t units = a.N * nb;
+        const int grid = grid_for(k, kBlock, smem_bytes<T>(), (units + kWarps - 1) / kWarps);
+        const uint32_t nwarps = (uint32_t)grid * kWarps;
+        p.step_n = nwarps / p.nb;
+        p.step_j = nwarps % p.nb;
+        quantize_fast_kernel<T, kStats><<<grid, kBlock, smem_bytes<T>(), s>>>(p);
     } else {
+        GParams p;
+        p.x = a.x;
+        p.N = a.N;
+        p.D = a.D;
+        p.ng = a.ng;
+        p.sample_base = a.sample_base;
+        p.bits = a.bits;
+        p.off = a.off;
+        p.gmin = a.gmin;
+        p.gmax = a.gmax;
+        p.packed = a.packed;
+        p.zmin = a.zmin;
+        p.scale = a.scale;
+        p.rk = make_round_keys(a.seed);
         const void* k = (const void*)quantize_generic_kernel<T, kStats>;
-        const int grid = grid_for(k, kBlock, 0, (a.N * a.ng + 7) / 8);
+        const int grid = grid_for(k, kBlock, 0, (a.N * a.ng + kWarps - 1) / kWarps);
         quantize_generic_kernel<T, kStats><<<grid, kBlock, 0, s>>>(p);
     }
     return cudaGetLastError();

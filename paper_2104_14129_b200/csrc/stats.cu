@@ -1,4 +1,4 @@
-// stats.cu -- K1 group_stats + K1b sens_reduce: pass 1 of the mixed-precision
+// stats.cu -- K1 group_stats (with K1b sens_reduce fused): pass 1 of the mixed-precision
 // path.  Per group the canonical min Z and max M; per sample the
 // range norm S_n = ||R_n||^2 (the ||R_n||^2 factor of w_n in Eq. 7),
 // summed in ACTNN-Q v1's canonical order O11 so that the allocator sees the
@@ -9,7 +9,9 @@
 //       writes them coalesced and runs the fp64 xor butterfly over
 //       v_l = R_l^2 (lane l = group l; zero past the sample's last group):
 //       T_{n,c} = v_0 after v_l <- v_l + v_{l^o}, o = 16, 8, 4, 2, 1.
-//   K1b: S_n = ((0 + T_{n,0}) + T_{n,1}) + ... in chunk order.
+//   K1b: S_n = ((0 + T_{n,0}) + T_{n,1}) + ... in chunk order, run by the
+//       last CTA to finish (an atomicInc ticket in the workspace that wraps
+//       back to 0, so no reset launch is needed) -- one launch per tensor.
 #include "device.cuh"
 #include "launch.h"
 
@@ -26,6 +28,8 @@ struct SParams {
     float* gmin;
     float* gmax;
     double* T;
+    double* sens;
+    unsigned int* ticket;  // zero before the first call; left zero by every call
 };
 
 template <typename T, bool kFast>
@@ -105,24 +109,30 @@ __global__ void __launch_bounds__(kBlock) group_stats_kernel(SParams p) {
             }
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
-            if (lane == 0) p.T[t] = v;
+            if (lane == 0) p.T[c * p.N + n] = v;  // chunk-major: coalesced in K1b
         }
         __syncthreads();
     }
-}
-
-__global__ void sens_reduce_kernel(const double* __restrict__ T, int64_t N, int64_t nch,
-                                   double* __restrict__ sens) {
-    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= N) return;
-    double s = 0.0;
-    for (int64_t c = 0; c < nch; ++c) s = __dadd_rn(s, T[n * nch + c]);
-    sens[n] = s;
+    // K1b fused: the last CTA sums every sample's chunk partials in order.
+    __shared__ unsigned int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicInc(p.ticket, gridDim.x - 1) == gridDim.x - 1);
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int64_t n = threadIdx.x; n < p.N; n += kBlock) {
+            double s = 0.0;
+            for (int64_t c = 0; c < p.nch; ++c) s = __dadd_rn(s, __ldcg(p.T + c * p.N + n));
+            p.sens[n] = s;
+        }
+    }
 }
 
 template <typename T>
 cudaError_t run(const StatsArgs& a, cudaStream_t s) {
-    SParams p{a.x, a.N, a.D, a.ng, a.nch, a.gmin, a.gmax, a.T};
+    SParams p{a.x, a.N, a.D, a.ng, a.nch, a.gmin, a.gmax, a.T, a.sens,
+              reinterpret_cast<unsigned int*>(a.T + a.N * a.nch)};
     const int64_t tiles = a.N * a.nch;
     if (a.fast) {
         const int grid = grid_for((const void*)group_stats_kernel<T, true>, kBlock, 0, tiles);
@@ -131,10 +141,6 @@ cudaError_t run(const StatsArgs& a, cudaStream_t s) {
         const int grid = grid_for((const void*)group_stats_kernel<T, false>, kBlock, 0, tiles);
         group_stats_kernel<T, false><<<grid, kBlock, 0, s>>>(p);
     }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    const int rb = 128;
-    sens_reduce_kernel<<<(unsigned)((a.N + rb - 1) / rb), rb, 0, s>>>(a.T, a.N, a.nch, a.sens);
     return cudaGetLastError();
 }
 

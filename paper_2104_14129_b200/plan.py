@@ -94,7 +94,7 @@ class ActivationSetPlan:
                 L.S_loc = (torch.zeros(N, dtype=torch.float64, device=dev) if nt != N
                            else L.S)
                 wsb = int(lib.actnn_workspace_bytes(OP_GROUP_STATS, N, D, G))
-                L.ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+                L.ws = torch.zeros(max(wsb, 8), dtype=torch.uint8, device=dev)
                 L.args["stats"] = (_p(x2), dt, N, D, G, _p(L.gmin), _p(L.gmax), _p(L.S_loc),
                                    _p(L.ws), L.ws.numel())
                 L.args["alloc"] = (_p(L.S), None, nt, budget, level_mask, D, G, _p(L.bits),
@@ -112,9 +112,9 @@ class ActivationSetPlan:
             L.args["dequant"] = (_p(L.packed), _p(L.zmin), _p(L.scale), bits_p, off_p, N, D, G)
             self.layers.append(L)
 
-    # launches per step: stats (2 kernels) + allocate + quantize + dequantize
+    # launches per step: stats (K1 with K1b fused) + allocate + quantize + dequantize
     def launches_per_step(self) -> int:
-        return len(self.layers) * (5 if self.mixed else 2)
+        return len(self.layers) * (4 if self.mixed else 2)
 
     def compress_layer(self, i: int, stream: ctypes.c_void_p, ev=None):
         lib, L = self.lib, self.layers[i]

@@ -37,8 +37,8 @@ def test_library_is_sm100a(lib):
 
 def test_abi_version_and_sizes(lib):
     assert lib.actnn_abi_version() == 1
-    assert lib.actnn_workspace_bytes(0, 4, 1024, 256) == 4 * 1 * 8
-    assert lib.actnn_workspace_bytes(0, 2, 256 * 33, 256) == 2 * 2 * 8
+    assert lib.actnn_workspace_bytes(0, 4, 1024, 256) == 4 * 1 * 8 + 8
+    assert lib.actnn_workspace_bytes(0, 2, 256 * 33, 256) == 2 * 2 * 8 + 8
     assert lib.actnn_workspace_bytes(1, 4, 1024, 256) == 0
     assert lib.actnn_packed_bytes(4, 1024, 256, None) == 4 * 4 * 256
     bits = np.array([1, 2, 4, 8], np.uint8)
