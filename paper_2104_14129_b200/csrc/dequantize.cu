@@ -114,7 +114,7 @@ __device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount, 
         dequant_unit<TO, b, false>(st, gcount, myZ, mySc, dst, lane);
 }
 
-template <typename TO>
+template <typename TO, bool kCached>
 __global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid_constant__ DParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
@@ -124,9 +124,8 @@ __global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid
     uint8_t* s_bits = smem + (size_t)kWarps * kS * kStage + (size_t)kWarps * kS * 8;
     uint32_t* s_off = reinterpret_cast<uint32_t*>(s_bits + kNCap);
 
-    const bool cached = p.N <= (uint32_t)kNCap;
     const int64_t off0 = p.off[0];
-    if (cached) {
+    if (kCached) {
         for (uint32_t i = threadIdx.x; i < p.N; i += kBlock) {
             s_bits[i] = p.bits[i];
             s_off[i] = (uint32_t)((p.off[i] - off0) >> 5);
@@ -150,9 +149,9 @@ __global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid
         }
     };
     auto gcount_of = [&](uint32_t j) { return (int)min((uint32_t)kU, p.ng - j * kU); };
-    auto width = [&](uint32_t n) { return cached ? (int)s_bits[n] : (int)p.bits[n]; };
+    auto width = [&](uint32_t n) { return kCached ? (int)s_bits[n] : (int)p.bits[n]; };
     auto seg_of = [&](uint32_t n, uint32_t j, int b) {
-        const int64_t sofs = cached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
+        const int64_t sofs = kCached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
         return p.packed + sofs + (uint64_t)j * (kU * 32) * b;
     };
     // lane 0 issues the bulk copy of unit (pn, pj) into stage s
@@ -264,17 +263,22 @@ cudaError_t run(const DequantArgs& a, cudaStream_t s) {
         p.ng = (uint32_t)a.ng;
         p.nb = (uint32_t)nb;
         p.out = a.out;
-        const void* k = (const void*)dequantize_fast_kernel<TO>;
-        static bool attr = false;
-        if (!attr) {
+        const bool cached = a.N <= kNCap;
+        const void* k = cached ? (const void*)dequantize_fast_kernel<TO, true>
+                               : (const void*)dequantize_fast_kernel<TO, false>;
+        static bool attr[2] = {false, false};
+        if (!attr[cached]) {
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-            attr = true;
+            attr[cached] = true;
         }
         const int grid = grid_for(k, kBlock, kSmem, (a.N * nb + kWarps - 1) / kWarps);
         const uint32_t nwarps = (uint32_t)grid * kWarps;
         p.step_n = nwarps / p.nb;
         p.step_j = nwarps % p.nb;
-        dequantize_fast_kernel<TO><<<grid, kBlock, kSmem, s>>>(p);
+        if (cached)
+            dequantize_fast_kernel<TO, true><<<grid, kBlock, kSmem, s>>>(p);
+        else
+            dequantize_fast_kernel<TO, false><<<grid, kBlock, kSmem, s>>>(p);
     } else {
         GDParams p{a.packed, a.zmin, a.scale, a.bits, a.off, a.N, a.D, a.ng, a.out};
         const int grid = grid_for((const void*)dequantize_generic_kernel<TO>, kBlock, 0,

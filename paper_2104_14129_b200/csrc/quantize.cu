@@ -205,7 +205,7 @@ __device__ __forceinline__ void quant_unit_any(const float (&v)[kU][8], int gcou
         quant_unit<b, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, rk, lane);
 }
 
-template <typename T, bool kStats>
+template <typename T, bool kStats, bool kCached>
 __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
     quantize_fast_kernel(const __grid_constant__ QParams p) {
     constexpr int S = Cfg<T>::S;
@@ -219,9 +219,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
     uint8_t* s_bits = smem + (size_t)kWarps * S * stage_bytes<T>() + (size_t)kWarps * S * 8;
     uint32_t* s_off = reinterpret_cast<uint32_t*>(s_bits + kNCap);
 
-    const bool cached = p.N <= (uint32_t)kNCap;
     const int64_t off0 = p.off[0];
-    if (cached) {
+    if (kCached) {
         for (uint32_t i = threadIdx.x; i < p.N; i += kBlock) {
             s_bits[i] = p.bits[i];
             s_off[i] = (uint32_t)((p.off[i] - off0) >> 5);  // offsets are multiples of 32 B
@@ -282,8 +281,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
             nMn = __ldg(p.gmin + g2);
             nMx = __ldg(p.gmax + g2);
         }
-        const int b = cached ? (int)s_bits[n] : (int)p.bits[n];
-        const int64_t sofs = cached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
+        const int b = kCached ? (int)s_bits[n] : (int)p.bits[n];
+        const int64_t sofs = kCached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
 
         mbar_wait(&bars[stage], phase);
         float v[kU][8];
@@ -291,6 +290,20 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
 #pragma unroll
         for (int k = 0; k < kU; ++k)
             if (k < gcount) lds8(st + k * kG + lane * 8, v[k]);
+        // Re-arm the stage with the unit S ahead as soon as it has been read, so
+        // S units stay in flight while this one is computed.  In-warp WAR: all
+        // lanes issued their shared loads before the __syncwarp; the new bulk
+        // copy first has to fetch from HBM (~1 us) before it writes the stage.
+        __syncwarp();
+        if (lane == 0) {
+            if (pn < p.N) {
+                const uint32_t bytes = (uint32_t)(gcount_of(pj) * kG * (int)sizeof(T));
+                mbar_expect_tx(&bars[stage], bytes);
+                bulk_g2s(ring + stage * SE, x + (uint64_t)pn * p.D + (uint64_t)pj * (kU * kG),
+                         bytes, &bars[stage]);
+            }
+            advance(pn, pj);
+        }
         if constexpr (kStats) {
 #pragma unroll
             for (int k = 0; k < kU; ++k) {
@@ -324,19 +337,6 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
             case 6: quant_unit<6, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
             case 7: quant_unit<7, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
             default: break;  // invalid width: outside the contract (ACTNN_CHECK=1 reports it)
-        }
-        // Every lane's reads of this stage were consumed above; re-arm it with the
-        // unit S ahead.  (In-warp WAR: the generic-proxy loads have completed, so
-        // the async-proxy write cannot overtake them.)
-        __syncwarp();
-        if (lane == 0) {
-            if (pn < p.N) {
-                const uint32_t bytes = (uint32_t)(gcount_of(pj) * kG * (int)sizeof(T));
-                mbar_expect_tx(&bars[stage], bytes);
-                bulk_g2s(ring + stage * SE, x + (uint64_t)pn * p.D + (uint64_t)pj * (kU * kG),
-                         bytes, &bars[stage]);
-            }
-            advance(pn, pj);
         }
         if (++stage == S) {
             stage = 0;
@@ -432,19 +432,24 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
         p.zmin = a.zmin;
         p.scale = a.scale;
         p.rk = make_round_keys(a.seed);
-        const void* k = (const void*)quantize_fast_kernel<T, kStats>;
-        static bool attr = false;  // one-time opt-in above 48 KB of dynamic smem
-        if (!attr) {
+        const bool cached = a.N <= kNCap;
+        const void* k = cached ? (const void*)quantize_fast_kernel<T, kStats, true>
+                               : (const void*)quantize_fast_kernel<T, kStats, false>;
+        static bool attr[2] = {false, false};  // one-time opt-in above 48 KB of dynamic smem
+        if (!attr[cached]) {
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes<T>());
-            attr = true;
+            attr[cached] = true;
         }
         const int64_t units = a.N * nb;
         const int grid = grid_for(k, kBlock, smem_bytes<T>(), (units + kWarps - 1) / kWarps);
         const uint32_t nwarps = (uint32_t)grid * kWarps;
         p.step_n = nwarps / p.nb;
         p.step_j = nwarps % p.nb;
-        quantize_fast_kernel<T, kStats><<<grid, kBlock, smem_bytes<T>(), s>>>(p);
+        if (cached)
+            quantize_fast_kernel<T, kStats, true><<<grid, kBlock, smem_bytes<T>(), s>>>(p);
+        else
+            quantize_fast_kernel<T, kStats, false><<<grid, kBlock, smem_bytes<T>(), s>>>(p);
     } else {
         GParams p;
         p.x = a.x;
