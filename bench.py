@@ -295,12 +295,19 @@ def main():
     sp = __import__("ctypes").c_void_p(stream.cuda_stream)
     nl = len(plan.layers)
 
+    side = torch.cuda.Stream(dev, priority=-1)   # stats/allocation chain (high priority)
+    aux = torch.cuda.Stream(dev)                  # second decompress stream
+
     def step(ev=None):
+        if ev is None:  # the timed schedule: two-stream software pipeline
+            plan.compress_all(stream, side)
+            plan.decompress_all(outs, out_dt, [stream, aux])
+            return
+        # breakdown: serial per-tensor launches, an event pair around each kernel
         for i in range(nl):
-            plan.compress_layer(i, sp, None if ev is None else ev[i])
+            plan.compress_layer(i, sp, ev[i])
         for i in range(nl):
-            plan.decompress_layer(i, outs[i & 1], out_dt, sp,
-                                  None if ev is None else ev[nl + i])
+            plan.decompress_layer(i, outs[i & 1], out_dt, sp, ev[nl + i])
 
     def barrier():
         if world > 1:
@@ -354,6 +361,20 @@ def main():
         kt[k] /= kb
     for k in tq:
         tq[k] /= kb
+    if os.environ.get("ACTNN_LAYER_DUMP") and rank == 0:
+        # per-tensor kernel times of the breakdown steps (diagnostics only)
+        rows = []
+        for i, L in enumerate(plan.layers):
+            rows.append({"layer": i, "name": wl.acts[i].name, "N": L.N, "D": L.D,
+                         "stats_us": 1e3 * sum(e[i][0].elapsed_time(e[i][1]) for e in evs) / kb
+                         if plan.mixed else None,
+                         "alloc_gap_us": 1e3 * sum(e[i][1].elapsed_time(e[i][2]) for e in evs) / kb
+                         if plan.mixed else None,
+                         "quant_us": 1e3 * sum(e[i][2].elapsed_time(e[i][3]) for e in evs) / kb,
+                         "dequant_us": 1e3 * sum(e[nl + i][0].elapsed_time(e[nl + i][1])
+                                                 for e in evs) / kb})
+        with open(os.environ["ACTNN_LAYER_DUMP"], "w") as f:
+            json.dump(rows, f, indent=0)
     bits_host = plan.bits_host()
     alg = algorithmic_bytes(plan.layers, bits_host, s_in, s_in, plan.mixed)
     peak, peak_src = hbm_peak()

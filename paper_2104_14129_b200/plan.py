@@ -141,6 +141,52 @@ class ActivationSetPlan:
         if ev is not None:
             ev[1].record()
 
+    # ------------------------------------------------------------ pipelined set
+    def _events(self):
+        if getattr(self, "_evs", None) is None:
+            self._evs = [torch.cuda.Event() for _ in self.layers]
+        return self._evs
+
+    def compress_all(self, main: torch.cuda.Stream, side: torch.cuda.Stream):
+        """Compress every tensor, software-pipelined over two streams: the
+        stats -> [all-gather] -> allocation chain of tensor l runs on `side`
+        (high priority) while `main` quantises tensor l-1, so the single-CTA
+        allocator and the kernels' ramp-up/tail overlap other work.  `main`
+        waits on an event per tensor; every output is ready on `main` on return."""
+        if not self.mixed:
+            sp = _P(main.cuda_stream)
+            for i in range(len(self.layers)):
+                _lib.check(self.lib.actnn_quantize(*self.layers[i].args["quant"], sp))
+            return
+        lib, evs = self.lib, self._events()
+        side.wait_stream(main)
+        ss, sm = _P(side.cuda_stream), _P(main.cuda_stream)
+        for i, L in enumerate(self.layers):
+            _lib.check(lib.actnn_group_stats(*L.args["stats"], ss))
+            if self.gather is not None:
+                with torch.cuda.stream(side):
+                    self.gather(L.S, L.S_loc)
+            _lib.check(lib.actnn_allocate_bits(*L.args["alloc"], ss))
+            evs[i].record(side)
+        for i, L in enumerate(self.layers):
+            main.wait_event(evs[i])
+            _lib.check(lib.actnn_quantize(*L.args["quant"], sm))
+
+    def decompress_all(self, outs: Sequence[torch.Tensor], out_dt: int,
+                       streams: Sequence[torch.cuda.Stream]):
+        """Decompress every tensor into outs[i % len(outs)], alternating streams
+        so that one tensor's tail overlaps the next one's ramp-up; streams[0]
+        waits for the others on return."""
+        k = len(streams)
+        for s in streams[1:]:
+            s.wait_stream(streams[0])
+        sps = [_P(s.cuda_stream) for s in streams]
+        for i, L in enumerate(self.layers):
+            _lib.check(self.lib.actnn_dequantize(*L.args["dequant"], _p(outs[i % len(outs)]),
+                                                 out_dt, sps[i % k]))
+        for s in streams[1:]:
+            streams[0].wait_stream(s)
+
     def bits_host(self):
         lo = self.sample_base
         return [L.bits[lo:lo + L.N].cpu() if L.bits.numel() != L.N else L.bits.cpu()
