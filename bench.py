@@ -295,12 +295,13 @@ def main():
     sp = __import__("ctypes").c_void_p(stream.cuda_stream)
     nl = len(plan.layers)
 
-    side = torch.cuda.Stream(dev, priority=-1)   # stats/allocation chain (high priority)
+    side = torch.cuda.Stream(dev)                 # stats chain
+    alloc_s = torch.cuda.Stream(dev, priority=-1) # per-tensor allocation (high priority)
     aux = torch.cuda.Stream(dev)                  # second decompress stream
 
     def step(ev=None):
         if ev is None:  # the timed schedule: two-stream software pipeline
-            plan.compress_all(stream, side)
+            plan.compress_all(stream, side, alloc_s)
             plan.decompress_all(outs, out_dt, [stream, aux])
             return
         # breakdown: serial per-tensor launches, an event pair around each kernel

@@ -147,29 +147,38 @@ class ActivationSetPlan:
             self._evs = [torch.cuda.Event() for _ in self.layers]
         return self._evs
 
-    def compress_all(self, main: torch.cuda.Stream, side: torch.cuda.Stream):
-        """Compress every tensor, software-pipelined over two streams: the
-        stats -> [all-gather] -> allocation chain of tensor l runs on `side`
-        (high priority) while `main` quantises tensor l-1, so the single-CTA
-        allocator and the kernels' ramp-up/tail overlap other work.  `main`
-        waits on an event per tensor; every output is ready on `main` on return."""
+    def compress_all(self, main: torch.cuda.Stream, side: torch.cuda.Stream,
+                     alloc: Optional[torch.cuda.Stream] = None):
+        """Compress every tensor, software-pipelined over streams: the stats
+        kernels run back to back on `side`; tensor l's [all-gather ->]
+        allocation runs on `alloc` (high priority) once its stats are done, and
+        `main` quantises tensor l once its allocation is done.  The single-CTA
+        allocator and every kernel's ramp-up/tail overlap other tensors' work.
+        Every output is ready on `main` on return."""
         if not self.mixed:
             sp = _P(main.cuda_stream)
             for i in range(len(self.layers)):
                 _lib.check(self.lib.actnn_quantize(*self.layers[i].args["quant"], sp))
             return
-        lib, evs = self.lib, self._events()
+        lib = self.lib
+        if getattr(self, "_evs2", None) is None:
+            self._evs2 = [(torch.cuda.Event(), torch.cuda.Event()) for _ in self.layers]
+        alloc = alloc if alloc is not None else side
         side.wait_stream(main)
-        ss, sm = _P(side.cuda_stream), _P(main.cuda_stream)
+        ss, sa, sm = (_P(side.cuda_stream), _P(alloc.cuda_stream), _P(main.cuda_stream))
         for i, L in enumerate(self.layers):
+            ev_stats, ev_alloc = self._evs2[i]
             _lib.check(lib.actnn_group_stats(*L.args["stats"], ss))
+            if alloc is not side:
+                ev_stats.record(side)
+                alloc.wait_event(ev_stats)
             if self.gather is not None:
-                with torch.cuda.stream(side):
+                with torch.cuda.stream(alloc):
                     self.gather(L.S, L.S_loc)
-            _lib.check(lib.actnn_allocate_bits(*L.args["alloc"], ss))
-            evs[i].record(side)
+            _lib.check(lib.actnn_allocate_bits(*L.args["alloc"], sa))
+            ev_alloc.record(alloc)
         for i, L in enumerate(self.layers):
-            main.wait_event(evs[i])
+            main.wait_event(self._evs2[i][1])
             _lib.check(lib.actnn_quantize(*L.args["quant"], sm))
 
     def decompress_all(self, outs: Sequence[torch.Tensor], out_dt: int,
