@@ -265,10 +265,17 @@ def main():
     from paper_2104_14129_b200 import workloads as W
     from paper_2104_14129_b200.plan import ActivationSetPlan
 
+    # one process per GPU; ACTNN_DIST_BACKEND=gloo is a test mode in which
+    # several ranks may share a GPU (NCCL refuses duplicate devices)
+    backend = os.environ.get("ACTNN_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     wl = W.workload(args.config)
     n_loc = wl.N // world if args.config == "c5" else wl.N
@@ -284,7 +291,10 @@ def main():
     gather = None
     if world > 1:
         def gather(S, S_loc):
-            dist.all_gather_into_tensor(S, S_loc)
+            if backend == "nccl":
+                dist.all_gather_into_tensor(S, S_loc)
+            else:  # gloo (test mode: several ranks sharing one GPU)
+                dist.all_gather(list(S.view(world, -1).unbind(0)), S_loc)
     plan = ActivationSetPlan(xs, [W.quant_seed(t) for t in range(len(wl.acts))],
                              avg_bits=wl.avg_bits, bits=None if wl.avg_bits else wl.bits,
                              n_total=n_total, sample_base=rank * n_loc, gather=gather)
@@ -312,7 +322,7 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         torch.cuda.synchronize()
 
     for _ in range(max(3, args.warmup)):
@@ -330,7 +340,8 @@ def main():
         barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms], dtype=torch.float64,
+                          device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
@@ -400,7 +411,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist,
-                      s_in, E_loc, barrier)
+                      s_in, E_loc, barrier, backend)
 
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
@@ -428,7 +439,7 @@ def main():
 
 
 def run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist, s_in,
-            E_loc, barrier):
+            E_loc, barrier, backend="nccl"):
     """Host-pinned inputs copied in, compressed, decompressed and copied back
     out every step (per-tensor pipeline over three streams)."""
     import psutil
@@ -479,7 +490,8 @@ def run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, 
     barrier()
     ms = e0.elapsed_time(e1) / sample
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms], dtype=torch.float64,
+                          device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     return {"value": world * E_loc * s_in / (ms * 1e-3) / 1e9, "unit": "GB/s",

@@ -1,14 +1,16 @@
 // dequantize.cu -- K4: unpacker + dequantiser ("During
 // back-propagation, the activation is dequantized as h_hat = u_hat R/B + Z"),
 // ACTNN-Q v1 step O10.  Mirrors K3: a warp's unit is 4 consecutive groups of
-// one sample; the unit's packed bytes (contiguous: 4 x 32 b bytes) arrive by
-// cp.async.bulk in a per-warp ring of S shared-memory stages (lane 0 keeps S
-// units in flight); lane l reads the b bytes holding its 8 codes from shared
-// memory and writes its 8 consecutive outputs with one 256-bit (fp32) or
-// 128-bit (bf16) store, so each warp store covers whole 32 B sectors.
-// (float)code uses the exact 2^23 magic; the dequantisation is one
-// __ffma2_rn per element pair (single rounding, O10).  The per-group (Z,
-// scale) pairs are loaded lane-parallel and broadcast by shuffles.
+// one sample.  Everything the unit reads -- its packed bytes (contiguous:
+// 4 x 32 b bytes) and, when the tensor's metadata is 16-byte aligned per unit
+// (ng % 4 == 0), its 4 zero points and 4 scales -- arrives by cp.async.bulk
+// (TMA, SASS UBLKCP) in a per-warp ring of S shared-memory stages; lane 0 keeps
+// S units in flight and no global load is left on the warp's critical path.
+// Lane l reads the b bytes holding its 8 codes from shared memory (the (Z,
+// scale) pairs are broadcast reads) and writes its 8 consecutive outputs with
+// one 256-bit (fp32) or 128-bit (bf16) store, so each warp store covers whole
+// 32 B sectors.  (float)code uses the exact 2^23 magic; dequantisation is one
+// __ffma2_rn per element pair (single rounding, O10).
 #include "device.cuh"
 #include "launch.h"
 
@@ -18,10 +20,10 @@ namespace {
 constexpr int kU = 4;
 constexpr int kWarps = 8;
 constexpr int kBlock = kWarps * 32;
-constexpr int kS = 4;                    // stages per warp
-constexpr int kStage = kU * 32 * 8;      // bytes: 4 groups at the widest (b = 8)
+constexpr int kS = 4;                     // stages per warp
+constexpr int kPay = kU * 32 * 8;         // payload bytes at the widest (b = 8)
+constexpr int kStage = kPay + 32;         // + 4 zero points + 4 scales
 constexpr int kNCap = 2048;
-constexpr unsigned kFull = 0xffffffffu;
 constexpr size_t kSmem = (size_t)kWarps * kS * kStage + (size_t)kWarps * kS * 8 + kNCap +
                          4 * (kNCap + 1);
 
@@ -76,46 +78,52 @@ __device__ __forceinline__ uint32_t magic_code(uint64_t pay, int j) {
     }
 }
 
-template <typename TO, int b, bool kFullUnit>
-__device__ __forceinline__ void dequant_unit(const uint8_t* st, int gcount, float myZ,
-                                             float mySc, TO* dst, int lane) {
-    uint64_t pay[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-        if (kFullUnit || u < gcount) pay[u] = stage_payload<b>(st + u * 32 * b, lane);
+// One group: the lane's 8 codes -> 8 outputs, one vector store.
+template <typename TO, int b>
+__device__ __forceinline__ void dequant_group(uint64_t pay, float Z, float s, TO* dst) {
     const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
+    const float2 zz = make_float2(Z, Z), ss = make_float2(s, s);
+    float o[8];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        float2 c = make_float2(__uint_as_float(magic_code<b>(pay, 2 * p)),
+                               __uint_as_float(magic_code<b>(pay, 2 * p + 1)));
+        c = __fadd2_rn(c, m23);     // exact: (float)code
+        c = __ffma2_rn(c, ss, zz);  // code * scale + Z, one rounding
+        o[2 * p] = c.x;
+        o[2 * p + 1] = c.y;
+    }
+    store8(dst, o);
+}
+
+// A unit: zq/sq point at the 4 zero points / scales (shared memory when they
+// came with the stage, global otherwise).
+template <typename TO, int b, bool kFullUnit>
+__device__ __forceinline__ void dequant_unit(const uint8_t* st, int gcount, const float* zq,
+                                             const float* sq, TO* dst, int lane) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
         if (kFullUnit || u < gcount) {
-            const float Z = __shfl_sync(kFull, myZ, u);
-            const float s = __shfl_sync(kFull, mySc, u);
-            const float2 zz = make_float2(Z, Z), ss = make_float2(s, s);
-            float o[8];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                float2 c = make_float2(__uint_as_float(magic_code<b>(pay[u], 2 * p)),
-                                       __uint_as_float(magic_code<b>(pay[u], 2 * p + 1)));
-                c = __fadd2_rn(c, m23);          // exact: (float)code
-                c = __ffma2_rn(c, ss, zz);       // code * scale + Z, one rounding
-                o[2 * p] = c.x;
-                o[2 * p + 1] = c.y;
-            }
-            store8(dst + u * kG + lane * 8, o);
+            const uint64_t pay = stage_payload<b>(st + u * 32 * b, lane);
+            dequant_group<TO, b>(pay, zq[u], sq[u], dst + u * kG + lane * 8);
         }
     }
 }
 
 template <typename TO, int b>
-__device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount, float myZ,
-                                                 float mySc, TO* dst, int lane) {
+__device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount, const float* zq,
+                                                 const float* sq, TO* dst, int lane) {
     if (gcount == kU)
-        dequant_unit<TO, b, true>(st, gcount, myZ, mySc, dst, lane);
+        dequant_unit<TO, b, true>(st, gcount, zq, sq, dst, lane);
     else
-        dequant_unit<TO, b, false>(st, gcount, myZ, mySc, dst, lane);
+        dequant_unit<TO, b, false>(st, gcount, zq, sq, dst, lane);
 }
 
-template <typename TO, bool kCached>
-__global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid_constant__ DParams p) {
+// kCached: (bits, off) of all samples in shared memory (N <= kNCap).
+// kMeta: the unit's (zmin, scale) travel in the stage (ng % 4 == 0).
+template <typename TO, bool kCached, bool kMeta>
+__global__ void __launch_bounds__(kBlock, 3)
+    dequantize_fast_kernel(const __grid_constant__ DParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
@@ -150,17 +158,22 @@ __global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid
     };
     auto gcount_of = [&](uint32_t j) { return (int)min((uint32_t)kU, p.ng - j * kU); };
     auto width = [&](uint32_t n) { return kCached ? (int)s_bits[n] : (int)p.bits[n]; };
-    auto seg_of = [&](uint32_t n, uint32_t j, int b) {
-        const int64_t sofs = kCached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
-        return p.packed + sofs + (uint64_t)j * (kU * 32) * b;
-    };
-    // lane 0 issues the bulk copy of unit (pn, pj) into stage s
+    // lane 0: bulk copies of unit (pn, pj) into stage s
     auto issue = [&](uint32_t pn, uint32_t pj, int s) {
         int b = width(pn);
-        if (b < 1 || b > 8) b = 1;  // outside the contract; keep the ring's phases consistent
+        if (b < 1 || b > 8) b = 1;  // outside the contract; keeps the ring's phases consistent
+        const int64_t sofs = kCached ? ((int64_t)s_off[pn] << 5) : (p.off[pn] - off0);
         const uint32_t bytes = (uint32_t)(gcount_of(pj) * 32 * b);
-        mbar_expect_tx(&bars[s], bytes);
-        bulk_g2s(ring + s * kStage, seg_of(pn, pj, b), bytes, &bars[s]);
+        uint8_t* dst = ring + s * kStage;
+        if (kMeta) {
+            const uint32_t g = pn * p.ng + pj * kU;
+            mbar_expect_tx(&bars[s], bytes + 32);
+            bulk_g2s(dst + kPay, p.zmin + g, 16, &bars[s]);
+            bulk_g2s(dst + kPay + 16, p.scale + g, 16, &bars[s]);
+        } else {
+            mbar_expect_tx(&bars[s], bytes);
+        }
+        bulk_g2s(dst, p.packed + sofs + (uint64_t)pj * (kU * 32) * b, bytes, &bars[s]);
     };
 
     uint32_t pn = gw / p.nb, pj = gw % p.nb;
@@ -172,37 +185,26 @@ __global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid
             advance(pn, pj);
         }
     }
-    float nZ = 0.0f, nSc = 0.0f;  // lane u: (Z, scale) of group u of the current unit
-    if (n < p.N && lane < gcount_of(j)) {
-        const uint32_t g = n * p.ng + j * kU + lane;
-        nZ = __ldg(p.zmin + g);
-        nSc = __ldg(p.scale + g);
-    }
     int stage = 0;
     uint32_t phase = 0;
     while (n < p.N) {
         const int gcount = gcount_of(j);
-        const float myZ = nZ, mySc = nSc;
-        uint32_t nn = n, nj = j;
-        advance(nn, nj);
-        if (nn < p.N && lane < gcount_of(nj)) {  // prefetch the next unit's metadata
-            const uint32_t g2 = nn * p.ng + nj * kU + lane;
-            nZ = __ldg(p.zmin + g2);
-            nSc = __ldg(p.scale + g2);
-        }
         const int b = width(n);
         TO* dst = out + (uint64_t)n * p.D + (uint64_t)j * (kU * kG);
         const uint8_t* st = ring + stage * kStage;
+        const uint32_t g = n * p.ng + j * kU;
+        const float* zq = kMeta ? reinterpret_cast<const float*>(st + kPay) : p.zmin + g;
+        const float* sq = kMeta ? reinterpret_cast<const float*>(st + kPay + 16) : p.scale + g;
         mbar_wait(&bars[stage], phase);
-        if (b == 2) dequant_unit_any<TO, 2>(st, gcount, myZ, mySc, dst, lane);
-        else if (b == 1) dequant_unit_any<TO, 1>(st, gcount, myZ, mySc, dst, lane);
-        else if (b == 4) dequant_unit_any<TO, 4>(st, gcount, myZ, mySc, dst, lane);
-        else if (b == 8) dequant_unit_any<TO, 8>(st, gcount, myZ, mySc, dst, lane);
-        else if (b == 3) dequant_unit<TO, 3, false>(st, gcount, myZ, mySc, dst, lane);
-        else if (b == 5) dequant_unit<TO, 5, false>(st, gcount, myZ, mySc, dst, lane);
-        else if (b == 6) dequant_unit<TO, 6, false>(st, gcount, myZ, mySc, dst, lane);
-        else if (b == 7) dequant_unit<TO, 7, false>(st, gcount, myZ, mySc, dst, lane);
-        // the stage's loads were consumed by the stores above: re-arm it
+        if (b == 2) dequant_unit_any<TO, 2>(st, gcount, zq, sq, dst, lane);
+        else if (b == 1) dequant_unit_any<TO, 1>(st, gcount, zq, sq, dst, lane);
+        else if (b == 4) dequant_unit_any<TO, 4>(st, gcount, zq, sq, dst, lane);
+        else if (b == 8) dequant_unit_any<TO, 8>(st, gcount, zq, sq, dst, lane);
+        else if (b == 3) dequant_unit<TO, 3, false>(st, gcount, zq, sq, dst, lane);
+        else if (b == 5) dequant_unit<TO, 5, false>(st, gcount, zq, sq, dst, lane);
+        else if (b == 6) dequant_unit<TO, 6, false>(st, gcount, zq, sq, dst, lane);
+        else if (b == 7) dequant_unit<TO, 7, false>(st, gcount, zq, sq, dst, lane);
+        // the stage's shared loads were consumed by the stores above: re-arm it
         __syncwarp();
         if (lane == 0) {
             if (pn < p.N) issue(pn, pj, stage);
@@ -212,8 +214,7 @@ __global__ void __launch_bounds__(kBlock, 3) dequantize_fast_kernel(const __grid
             stage = 0;
             phase ^= 1u;
         }
-        n = nn;
-        j = nj;
+        advance(n, j);
     }
 }
 
@@ -240,11 +241,27 @@ __global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(const __grid
         const uint32_t mask = (1u << b) - 1u;
         TO* dst = out + n * p.D + i * kG;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int idx = lane * 8 + j;
-            if (idx < len) store1(dst + idx, dequant1((uint32_t)(pay >> (b * j)) & mask, s, Z));
+        for (int jj = 0; jj < 8; ++jj) {
+            const int idx = lane * 8 + jj;
+            if (idx < len) store1(dst + idx, dequant1((uint32_t)(pay >> (b * jj)) & mask, s, Z));
         }
     }
+}
+
+template <typename TO, bool kCached, bool kMeta>
+void launch_fast(const DParams& p0, int64_t units, cudaStream_t s) {
+    const void* k = (const void*)dequantize_fast_kernel<TO, kCached, kMeta>;
+    static bool attr = false;  // one-time opt-in above 48 KB of dynamic smem
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+        attr = true;
+    }
+    DParams p = p0;
+    const int grid = grid_for(k, kBlock, kSmem, (units + kWarps - 1) / kWarps);
+    const uint32_t nwarps = (uint32_t)grid * kWarps;
+    p.step_n = nwarps / p.nb;
+    p.step_j = nwarps % p.nb;
+    dequantize_fast_kernel<TO, kCached, kMeta><<<grid, kBlock, kSmem, s>>>(p);
 }
 
 template <typename TO>
@@ -262,23 +279,17 @@ cudaError_t run(const DequantArgs& a, cudaStream_t s) {
         p.D = (uint32_t)a.D;
         p.ng = (uint32_t)a.ng;
         p.nb = (uint32_t)nb;
+        p.step_n = p.step_j = 0;
         p.out = a.out;
         const bool cached = a.N <= kNCap;
-        const void* k = cached ? (const void*)dequantize_fast_kernel<TO, true>
-                               : (const void*)dequantize_fast_kernel<TO, false>;
-        static bool attr[2] = {false, false};
-        if (!attr[cached]) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-            attr[cached] = true;
-        }
-        const int grid = grid_for(k, kBlock, kSmem, (a.N * nb + kWarps - 1) / kWarps);
-        const uint32_t nwarps = (uint32_t)grid * kWarps;
-        p.step_n = nwarps / p.nb;
-        p.step_j = nwarps % p.nb;
-        if (cached)
-            dequantize_fast_kernel<TO, true><<<grid, kBlock, kSmem, s>>>(p);
-        else
-            dequantize_fast_kernel<TO, false><<<grid, kBlock, kSmem, s>>>(p);
+        // metadata by TMA: every unit's 4 floats start 16-byte aligned
+        const bool meta = (a.ng % kU == 0) && ((uintptr_t)a.zmin % 16 == 0) &&
+                          ((uintptr_t)a.scale % 16 == 0);
+        const int64_t units = a.N * nb;
+        if (cached && meta) launch_fast<TO, true, true>(p, units, s);
+        else if (cached) launch_fast<TO, true, false>(p, units, s);
+        else if (meta) launch_fast<TO, false, true>(p, units, s);
+        else launch_fast<TO, false, false>(p, units, s);
     } else {
         GDParams p{a.packed, a.zmin, a.scale, a.bits, a.off, a.N, a.D, a.ng, a.out};
         const int grid = grid_for((const void*)dequantize_generic_kernel<TO>, kBlock, 0,

@@ -372,3 +372,24 @@ def test_full_size_c4_layer_bf16_sampled(A, W):
     rng = np.random.default_rng(1)
     _check_sampled_groups(A, x, p, seed, 0, _sample_groups(rng, wl.N, act.D // 256, 128), out)
     assert int(host(p.bits).astype(np.int64).sum()) <= int(1.25 * wl.N)
+
+
+def test_compress_sharded_one_rank_nccl(A, W):
+    """dist.compress_sharded through a real (1-rank) NCCL group equals the
+    unsharded call byte for byte."""
+    import torch.distributed as dist
+    from paper_2104_14129_b200 import dist as AD
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    try:
+        act = W.resnet_activation_set(50)[12]
+        x = W.synth_activation(act, 8, 12, "f32", DEV)
+        a = AD.compress_sharded(x, 99, 2.0)
+        b = A.compress(x, seed=99, avg_bits=2.0)
+        torch.cuda.synchronize()
+        nb = int(host(b.off)[-1])
+        assert np.array_equal(host(a.packed[:nb]), host(b.packed[:nb]))
+        assert np.array_equal(host(a.bits), host(b.bits))
+    finally:
+        dist.destroy_process_group()
