@@ -54,6 +54,18 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(kernel_key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel, from
+    the committed ncu launch list of one C3 step (profiles/traffic.json)."""
+    name = {"stats": "group_stats_kernel", "quantize": "quantize_fast_kernel",
+            "dequantize": "dequantize_fast_kernel"}[kernel_key]
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)["kernels"][name]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------ clocks
 REASONS = [(0x4, "sw_power_cap"), (0x8, "hw_slowdown"), (0x20, "sw_thermal_slowdown"),
            (0x40, "hw_thermal_slowdown"), (0x80, "hw_power_brake_slowdown"),
@@ -397,7 +409,7 @@ def main():
                                            "quantize": "quantize_fast_kernel (K3)",
                                            "dequantize": "dequantize_fast_kernel (K4)"}[dom],
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "peak_source": peak_src, "traffic": None,
+                "peak_source": peak_src, "traffic": ncu_traffic(dom),
                 "algorithmic_bytes_per_launch": alg[dom] / launches_dom,
                 "avg_launch_us": kt[dom] * 1e3 / launches_dom,
                 "per_kernel": {k: {"ms_per_step": kt[k], "share_of_step": kt[k] / ms_step,
