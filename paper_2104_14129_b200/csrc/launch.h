@@ -60,6 +60,7 @@ struct AllocArgs {
 };
 
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
+cudaError_t launch_quantize_ws(const QuantArgs& a, cudaStream_t s);  // mixed-mode fast path
 cudaError_t launch_dequantize(const DequantArgs& a, cudaStream_t s);
 cudaError_t launch_group_stats(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s);

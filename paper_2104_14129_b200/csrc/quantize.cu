@@ -25,6 +25,8 @@
 //     by shuffles so every store is a word and the warp fills whole sectors.
 // Ragged D, unaligned x or huge tensors take the generic kernel (scalar loads,
 // one group per warp iteration); it produces exactly the same bytes.
+#include <cstdlib>
+
 #include "device.cuh"
 #include "launch.h"
 
@@ -36,18 +38,33 @@ constexpr int kWarps = 8;
 constexpr int kBlock = kWarps * 32;
 constexpr int kNCap = 2048;  // samples whose (bits, off) are cached in shared memory
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef ACTNN_Q_KEYS
+#define ACTNN_Q_KEYS 0
+#endif
 
 template <typename T>
 struct Cfg;
+#ifndef ACTNN_Q_S32
+#define ACTNN_Q_S32 3
+#endif
+#ifndef ACTNN_Q_MINB32
+#define ACTNN_Q_MINB32 2
+#endif
+#ifndef ACTNN_Q_S16
+#define ACTNN_Q_S16 4
+#endif
+#ifndef ACTNN_Q_MINB16
+#define ACTNN_Q_MINB16 3
+#endif
 template <>
 struct Cfg<float> {
-    static constexpr int S = 3;          // stages per warp (4 KB each)
-    static constexpr int MinBlocks = 2;  // CTAs per SM
+    static constexpr int S = ACTNN_Q_S32;          // stages per warp (4 KB each)
+    static constexpr int MinBlocks = ACTNN_Q_MINB32;  // CTAs per SM
 };
 template <>
 struct Cfg<uint16_t> {
-    static constexpr int S = 4;  // 2 KB each
-    static constexpr int MinBlocks = 3;
+    static constexpr int S = ACTNN_Q_S16;  // 2 KB each
+    static constexpr int MinBlocks = ACTNN_Q_MINB16;
 };
 
 template <typename T>
@@ -139,7 +156,11 @@ __device__ __forceinline__ void codes_wide(const float v[8], float Z, float inv1
 template <int b>
 __device__ __forceinline__ void quant_group(const float v[8], float Z, float inv14, uint64_t blk,
                                             const RoundKeys& rk, uint8_t* seg, int lane) {
+#if ACTNN_Q_KEYS == 1
+    const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk.k[0], rk.k[1]);
+#else
     const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+#endif
     if constexpr (b == 2) {
         const uint32_t pl = codes_small<2>(v, Z, inv14, o);
         const uint32_t q = __shfl_down_sync(kFull, pl, 1);
@@ -476,6 +497,10 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
 
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
     const bool stats = (a.gmin == nullptr);
+    const bool fits = a.N * a.ng < (1ll << 31) && a.D < (1ll << 31) &&
+                      a.sample_base + a.N < (1ll << 31);
+    // mixed path (group stats given): the warp-specialised kernel (quantize_ws.cu)
+    if (!stats && a.fast && fits && !std::getenv("ACTNN_NO_WS")) return launch_quantize_ws(a, s);
     if (a.dt == 0) return stats ? run<float, true>(a, s) : run<float, false>(a, s);
     return stats ? run<uint16_t, true>(a, s) : run<uint16_t, false>(a, s);
 }

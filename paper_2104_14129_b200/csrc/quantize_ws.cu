@@ -1,0 +1,388 @@
+// quantize_ws.cu -- K3 for the mixed-precision path (gmin/gmax from K1),
+// warp-specialised.  Same bytes as quantize.cu, ACTNN-Q v1 O4-O9.
+//
+// A CTA = kCons consumer warps + 1 producer warp.  Consumer warp w walks the
+// units u = (blockIdx * kCons + w) + r * nwarps (a unit = U consecutive groups
+// of one sample, 4 KB of input); it owns a ring of S shared-memory stages.
+// The producer warp, S rounds ahead of the consumers, for every consumer's
+// next unit:
+//   - waits until the consumer released the stage (empty mbarrier),
+//   - computes the unit's group constants lane-parallel (one group per lane
+//     per step: Z, inv14 = RN(B/R) 2^14, scale = RN(R/B), O3-O4) and stores
+//     zmin/scale to global,
+//   - writes a unit descriptor (packed segment offset, Philox block, width,
+//     group count, the U (Z, inv14) pairs) into the stage,
+//   - arrives on the stage's full mbarrier with the byte count and issues the
+//     cp.async.bulk (TMA) of the unit's input.
+// Consumers then only do the per-element work: shared loads, one Philox call
+// per group, fixed-point SR codes, packing and word stores.  Moving the unit
+// walk, the divisions and the metadata traffic to one warp amortises them over
+// kCons * U groups per producer step instead of U per consumer step.
+#include "device.cuh"
+#include "launch.h"
+
+namespace actnn {
+namespace {
+
+#ifndef ACTNN_WS_CONS
+#define ACTNN_WS_CONS 8
+#endif
+#ifndef ACTNN_WS_S
+#define ACTNN_WS_S 3
+#endif
+#ifndef ACTNN_WS_MINB
+#define ACTNN_WS_MINB 2
+#endif
+constexpr int kCons = ACTNN_WS_CONS;      // consumer warps per CTA
+constexpr int kThreads = (kCons + 1) * 32;
+constexpr int kS = ACTNN_WS_S;            // stages per consumer
+constexpr int kUnitBytes = 4096;          // one TMA copy per unit
+constexpr int kNCap = 2048;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T>
+struct WS {
+    static constexpr int U = kUnitBytes / (kG * (int)sizeof(T));  // groups per unit: 4 / 8
+    static constexpr int SE = kUnitBytes / (int)sizeof(T);        // elements per stage
+};
+
+struct __align__(16) Desc {
+    uint64_t seg;   // byte offset of the unit's first group segment in `packed`
+    uint64_t blk0;  // Philox block of lane 0 of the unit's first group
+    uint32_t b;     // width
+    uint32_t gcount;
+    uint32_t pad[2];
+    float Z[8];
+    float inv[8];
+};
+
+template <typename T>
+__host__ __device__ constexpr size_t ws_smem_bytes() {
+    return (size_t)kCons * kS * kUnitBytes + (size_t)kCons * kS * sizeof(Desc) +
+           (size_t)kCons * kS * 16 + kNCap + 4 * (kNCap + 1);
+}
+
+struct WSParams {
+    const void* x;
+    uint32_t N, D, ng, nb;
+    uint32_t step_n, step_j;  // unit stride of a consumer: nwarps = step_n * nb + step_j
+    uint32_t sample_base;
+    const uint8_t* bits;
+    const int64_t* off;
+    const float* gmin;
+    const float* gmax;
+    uint8_t* packed;
+    float* zmin;
+    float* scale;
+    RoundKeys rk;
+};
+
+// Raise the expected transaction count without arriving (the arrive comes
+// after the descriptor is written).
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int b>
+__device__ __forceinline__ uint32_t ws_codes_small(const float v[8], float Z, float inv14,
+                                                   const Philox4& o) {
+    const float2 nz = make_float2(-Z, -Z);
+    const float2 iv = make_float2(inv14, inv14);
+    const float2 mg = make_float2(12582912.0f, 12582912.0f);
+    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+    uint32_t acc = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
+        const float2 t = __ffma2_rn(d, iv, mg);
+        uint32_t T = __float_as_uint(t.y) * 65536u + __float_as_uint(t.x);
+        T = T + (w[p] & 0x3FFF3FFFu) - 0x4B400000u;
+        if (b == 2)
+            acc |= __umulhi(T & 0xC000C000u, (1u << (18 + 4 * p)) + (1u << (4 + 4 * p)));
+        else
+            acc |= __umulhi(T & 0x40004000u, (1u << (18 + 2 * p)) + (1u << (3 + 2 * p)));
+    }
+    return acc & ((1u << (8 * b)) - 1u);
+}
+
+// Codes of one group at width b from its Philox draw, packed and stored
+// (ACTNN-Q v1 O5-O8; the same arithmetic as quantize.cu).
+template <int b>
+__device__ __forceinline__ void ws_store(const float v[8], float Z, float inv14,
+                                         const Philox4& o, uint8_t* seg, int lane) {
+    if constexpr (b == 2) {
+        const uint32_t pl = ws_codes_small<2>(v, Z, inv14, o);
+        const uint32_t q = __shfl_down_sync(kFull, pl, 1);
+        if (!(lane & 1)) *reinterpret_cast<uint32_t*>(seg + lane * 2) = pl | (q << 16);
+    } else if constexpr (b == 1) {
+        const uint32_t pl = ws_codes_small<1>(v, Z, inv14, o);
+        const uint32_t q1 = __shfl_down_sync(kFull, pl, 1);
+        const uint32_t q2 = __shfl_down_sync(kFull, pl, 2);
+        const uint32_t q3 = __shfl_down_sync(kFull, pl, 3);
+        if (!(lane & 3))
+            *reinterpret_cast<uint32_t*>(seg + lane) = pl | (q1 << 8) | (q2 << 16) | (q3 << 24);
+    } else {
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+        uint32_t code[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t r = ((j & 1) ? (w[j >> 1] >> 16) : w[j >> 1]) & 0x3FFFu;
+            code[j] = sr_code(v[j], Z, inv14, r);
+        }
+        if constexpr (b == 8) {
+            const uint32_t lo = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
+            const uint32_t hi = code[4] | (code[5] << 8) | (code[6] << 16) | (code[7] << 24);
+            *reinterpret_cast<uint2*>(seg + lane * 8) = make_uint2(lo, hi);
+        } else if constexpr (b == 4) {
+            uint32_t pl = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pl |= code[j] << (4 * j);
+            *reinterpret_cast<uint32_t*>(seg + lane * 4) = pl;
+        } else {
+            uint64_t pl = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pl |= (uint64_t)code[j] << (b * j);
+#pragma unroll
+            for (int t = 0; t < b; ++t) seg[lane * b + t] = (uint8_t)(pl >> (8 * t));
+        }
+    }
+}
+
+// One unit: read the stage and its descriptor, release the stage, then per
+// group one Philox call and the width-specific codes/store (a warp-uniform
+// branch per group, so the Philox and data code exists once).
+template <typename T>
+__device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* packed,
+                                        const RoundKeys& rk, int lane, uint64_t* empty) {
+    constexpr int U = WS<T>::U;
+    const int gcount = (int)d.gcount;
+    const int b = (int)d.b;
+    float v[U][8];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+        if (k < gcount) lds8(st + k * kG + lane * 8, v[k]);
+    const uint64_t seg0 = d.seg, blk0 = d.blk0;
+    float Zs[U], Is[U];  // the descriptor is rewritten once the stage is released
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        Zs[k] = d.Z[k];
+        Is[k] = d.inv[k];
+    }
+    // every lane's shared reads of this stage are issued: release it (the
+    // producer's next bulk copy into it first has to fetch from HBM)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty);
+    uint8_t* seg = packed + seg0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        if (k < gcount) {
+            const float Z = Zs[k], inv = Is[k];
+            const uint64_t blk = blk0 + (uint64_t)(k * 32 + lane);
+            const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+            uint8_t* sg = seg + k * 32 * b;
+            if (b == 2) ws_store<2>(v[k], Z, inv, o, sg, lane);
+            else if (b == 1) ws_store<1>(v[k], Z, inv, o, sg, lane);
+            else if (b == 4) ws_store<4>(v[k], Z, inv, o, sg, lane);
+            else if (b == 8) ws_store<8>(v[k], Z, inv, o, sg, lane);
+            else if (b == 3) ws_store<3>(v[k], Z, inv, o, sg, lane);
+            else if (b == 5) ws_store<5>(v[k], Z, inv, o, sg, lane);
+            else if (b == 6) ws_store<6>(v[k], Z, inv, o, sg, lane);
+            else if (b == 7) ws_store<7>(v[k], Z, inv, o, sg, lane);
+        }
+    }
+}
+
+template <typename T, bool kCached>
+__global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(const __grid_constant__ WSParams p) {
+    constexpr int U = WS<T>::U;
+    constexpr int SE = WS<T>::SE;
+    extern __shared__ __align__(128) uint8_t smem[];
+    T* ring = reinterpret_cast<T*>(smem);
+    Desc* desc = reinterpret_cast<Desc*>(smem + (size_t)kCons * kS * kUnitBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(desc + kCons * kS);
+    uint64_t* empty = full + kCons * kS;
+    uint8_t* s_bits = reinterpret_cast<uint8_t*>(empty + kCons * kS);
+    uint32_t* s_off = reinterpret_cast<uint32_t*>(s_bits + kNCap);
+
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int64_t off0 = p.off[0];
+    if (kCached) {
+        for (uint32_t i = threadIdx.x; i < p.N; i += kThreads) {
+            s_bits[i] = p.bits[i];
+            s_off[i] = (uint32_t)((p.off[i] - off0) >> 5);
+        }
+    }
+    if (threadIdx.x < kCons * kS) {
+        mbar_init(&full[threadIdx.x], 1);
+        mbar_init(&empty[threadIdx.x], 1);
+    }
+    fence_mbar_init();
+    __syncthreads();
+    const uint32_t nwarps = gridDim.x * kCons;
+
+    if (w == kCons) {
+        // ------------------------------------------------------------ producer
+        // lane l serves consumer c = l / (32 / kCons) ... generalised: each step
+        // covers kCons units x U groups with 32 lanes: a lane handles groups
+        // k = (l % LPC) + t * LPC of consumer c = l / LPC, LPC = 32 / kCons.
+        constexpr int LPC = 32 / kCons;        // lanes per consumer (4)
+        constexpr int GPL = U / LPC;           // groups per lane (1 or 2)
+        const int c = lane / LPC, kl = lane % LPC;
+        uint32_t u0 = blockIdx.x * kCons + c;
+        uint32_t n = u0 / p.nb, j = u0 % p.nb;
+        const T* __restrict__ x = static_cast<const T*>(p.x);
+        // (gmin, gmax) of this lane's groups, loaded one round ahead
+        auto load_meta = [&](uint32_t n_, uint32_t j_, float* mn, float* mx) {
+            const uint32_t gi = j_ * U;
+            const int gcount = (int)min((uint32_t)U, p.ng - gi);
+            const uint32_t g = n_ * p.ng + gi;
+#pragma unroll
+            for (int t = 0; t < GPL; ++t) {
+                const int k = kl + t * LPC;
+                mn[t] = k < gcount ? __ldg(p.gmin + g + k) : 0.0f;
+                mx[t] = k < gcount ? __ldg(p.gmax + g + k) : 0.0f;
+            }
+        };
+        float cmn[GPL], cmx[GPL];
+        if (n < p.N) load_meta(n, j, cmn, cmx);
+        for (uint32_t r = 0;; ++r) {
+            const bool valid = n < p.N;
+            if (!__any_sync(kFull, valid)) break;
+            const int s = (int)(r % kS);
+            const int slot = c * kS + s;
+            if (r >= (uint32_t)kS && valid && kl == 0)
+                mbar_wait(&empty[slot], ((r / kS) - 1) & 1);
+            __syncwarp();
+            const uint32_t gi = j * U;
+            const int gcount = (int)min((uint32_t)U, p.ng - gi);
+            if (valid && kl == 0) {  // the input copy first: it needs no metadata
+                const uint32_t bytes = (uint32_t)(gcount * kG * (int)sizeof(T));
+                mbar_expect_tx_only(&full[slot], bytes);
+                bulk_g2s(ring + (size_t)slot * SE, x + (uint64_t)n * p.D + (uint64_t)gi * kG, bytes,
+                         &full[slot]);
+            }
+            uint32_t nn = n + p.step_n, nj = j + p.step_j;
+            if (nj >= p.nb) {
+                nj -= p.nb;
+                ++nn;
+            }
+            float nmn[GPL], nmx[GPL];
+            if (nn < p.N) load_meta(nn, nj, nmn, nmx);
+            if (valid) {
+                const int b = kCached ? (int)s_bits[n] : (int)p.bits[n];
+                const uint32_t g = n * p.ng + gi;
+                Desc& d = desc[slot];
+#pragma unroll
+                for (int t = 0; t < GPL; ++t) {
+                    const int k = kl + t * LPC;
+                    if (k < gcount) {
+                        const GroupConst cc = group_const(cmn[t], cmx[t], b);
+                        p.zmin[g + k] = cc.Z;
+                        p.scale[g + k] = cc.scale;
+                        d.Z[k] = cc.Z;
+                        d.inv[k] = cc.inv14;
+                    }
+                }
+                if (kl == 0) {
+                    const int64_t sofs = kCached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
+                    d.seg = (uint64_t)sofs + (uint64_t)gi * 32 * b;
+                    d.blk0 = (uint64_t)(p.sample_base + n) * (p.D >> 3) + (uint64_t)gi * 32;
+                    d.b = (uint32_t)b;
+                    d.gcount = (uint32_t)gcount;
+                }
+            }
+            __syncwarp();  // descriptor writes of the consumer's lanes precede the arrive
+            if (valid && kl == 0) mbar_arrive(&full[slot]);
+            n = nn;
+            j = nj;
+#pragma unroll
+            for (int t = 0; t < GPL; ++t) {
+                cmn[t] = nmn[t];
+                cmx[t] = nmx[t];
+            }
+        }
+        return;
+    }
+
+    // -------------------------------------------------------------- consumers
+    uint32_t u0 = blockIdx.x * kCons + w;
+    uint32_t n = u0 / p.nb, j = u0 % p.nb;
+    int s = 0;
+    uint32_t ph = 0;
+    while (n < p.N) {
+        const int slot = w * kS + s;
+        mbar_wait(&full[slot], ph);
+        const Desc& d = desc[slot];
+        const T* st = ring + (size_t)slot * SE;
+        ws_unit<T>(st, d, p.packed, p.rk, lane, &empty[slot]);
+        if (++s == kS) {
+            s = 0;
+            ph ^= 1u;
+        }
+        n += p.step_n;
+        j += p.step_j;
+        if (j >= p.nb) {
+            j -= p.nb;
+            ++n;
+        }
+    }
+}
+
+template <typename T, bool kCached>
+void launch_ws(WSParams p, int64_t units, cudaStream_t s) {
+    const void* k = (const void*)quantize_ws_kernel<T, kCached>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ws_smem_bytes<T>());
+        attr = true;
+    }
+    const int grid = grid_for(k, kThreads, ws_smem_bytes<T>(), (units + kCons - 1) / kCons);
+    const uint32_t nwarps = (uint32_t)grid * kCons;
+    p.step_n = nwarps / p.nb;
+    p.step_j = nwarps % p.nb;
+    quantize_ws_kernel<T, kCached><<<grid, kThreads, ws_smem_bytes<T>(), s>>>(p);
+}
+
+template <typename T>
+cudaError_t run_ws(const QuantArgs& a, cudaStream_t s) {
+    constexpr int U = WS<T>::U;
+    WSParams p;
+    p.x = a.x;
+    p.N = (uint32_t)a.N;
+    p.D = (uint32_t)a.D;
+    p.ng = (uint32_t)a.ng;
+    p.nb = (uint32_t)((a.ng + U - 1) / U);
+    p.step_n = p.step_j = 0;
+    p.sample_base = (uint32_t)a.sample_base;
+    p.bits = a.bits;
+    p.off = a.off;
+    p.gmin = a.gmin;
+    p.gmax = a.gmax;
+    p.packed = a.packed;
+    p.zmin = a.zmin;
+    p.scale = a.scale;
+    p.rk = make_round_keys(a.seed);
+    const int64_t units = a.N * (int64_t)p.nb;
+    if (a.N <= kNCap)
+        launch_ws<T, true>(p, units, s);
+    else
+        launch_ws<T, false>(p, units, s);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// Mixed-mode fast path (gmin/gmax given, D % 256 == 0, aligned x, 32-bit walk).
+cudaError_t launch_quantize_ws(const QuantArgs& a, cudaStream_t s) {
+    return a.dt == 0 ? run_ws<float>(a, s) : run_ws<uint16_t>(a, s);
+}
+
+}  // namespace actnn

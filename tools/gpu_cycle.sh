@@ -11,5 +11,5 @@ d = json.loads(open("gpurun_out/bench_$TAG.log").read().strip().splitlines()[-1]
 print("value", round(d["value"], 1), "ms", round(d["ms_per_step"], 3), {k: (round(v["ms_per_step"], 3), round(v["frac"], 3)) for k, v in r["per_kernel"].items()})
 PY
 if [ "$LAYERS" != "none" ]; then
-timeout 800 ncu --set full --clock-control none --import-source on -k regex:"^quantize_fast|^dequantize_fast|^group_stats|^allocate" -s 4 -c 4 -o gpurun_out/prof_$TAG python tools/profile_step.py --steps 1 --layers $LAYERS > gpurun_out/ncu_$TAG.log 2>&1; echo ncu=$?
+timeout 800 ncu --set full --clock-control none --import-source on -k regex:"^quantize_|^dequantize_fast|^group_stats|^allocate" -s 4 -c 4 -o gpurun_out/prof_$TAG python tools/profile_step.py --steps 1 --layers $LAYERS > gpurun_out/ncu_$TAG.log 2>&1; echo ncu=$?
 fi

@@ -8,6 +8,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --log-file gpurun_out/${TAG}_launches.csv python tools/profile_step.py --steps 1 > gpurun_out/${TAG}_ncu_list.log 2>&1
 echo list=$?
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"^quantize_fast|^dequantize_fast|^group_stats|^allocate" -s 4 -c 4 \
+  -k regex:"^quantize_|^dequantize_fast|^group_stats|^allocate" -s 4 -c 4 \
   -o gpurun_out/${TAG}_full python tools/profile_step.py --steps 1 --layers 1 > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo full=$?
