@@ -321,10 +321,22 @@ def main():
     alloc_s = torch.cuda.Stream(dev, priority=-1) # per-tensor allocation (high priority)
     aux = torch.cuda.Stream(dev)                  # second decompress stream
 
+    phase_ev = []   # (start, mid, end) per step: compress / decompress split
+    flags = {"phases": False}
+
     def step(ev=None):
-        if ev is None:  # the timed schedule: two-stream software pipeline
+        record_phases = flags["phases"]
+        if ev is None:  # the timed schedule: software pipeline over streams
+            if record_phases:
+                marks = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                marks[0].record(stream)
             plan.compress_all(stream, side, alloc_s)
+            if record_phases:
+                marks[1].record(stream)
             plan.decompress_all(outs, out_dt, [stream, aux])
+            if record_phases:
+                marks[2].record(stream)
+                phase_ev.append(marks)
             return
         # breakdown: serial per-tensor launches, an event pair around each kernel
         for i in range(nl):
@@ -359,6 +371,16 @@ def main():
     ms_step = ms / args.steps
     E_loc = n_loc * sum(a.D for a in wl.acts)
     value = world * E_loc * s_in / (ms_step * 1e-3) / 1e9
+
+    # ---- the same schedule once more with events at the compress/decompress boundary
+    flags["phases"] = True
+    barrier()
+    for _ in range(min(args.steps, 5)):
+        step()
+    barrier()
+    flags["phases"] = False
+    t_comp = sum(m[0].elapsed_time(m[1]) for m in phase_ev) / len(phase_ev)
+    t_decomp = sum(m[1].elapsed_time(m[2]) for m in phase_ev) / len(phase_ev)
 
     # ---- per-kernel breakdown: same steps with an event pair around every launch
     kb = max(3, args.steps // 4)
@@ -431,8 +453,11 @@ def main():
             "vs_baseline": None, "dtype": wl.dtype,
             "data": "synthetic (seeded ResNet-shaped activations generated on the GPU)",
             "config": config_dict(wl, args, world, n_loc),
-            "compress_GBps": world * E_loc * s_in / (tq["compress"] * 1e-3) / 1e9,
-            "decompress_GBps": world * E_loc * s_in / (tq["decompress"] * 1e-3) / 1e9,
+            # phases of the pipelined schedule (events at the boundary; rank-local)
+            "compress_GBps": world * E_loc * s_in / (t_comp * 1e-3) / 1e9,
+            "decompress_GBps": world * E_loc * s_in / (t_decomp * 1e-3) / 1e9,
+            "compress_ms": t_comp, "decompress_ms": t_decomp,
+            "serial_breakdown_ms": {"compress": tq["compress"], "decompress": tq["decompress"]},
             "hbm_frac_step": total_alg / (ms_step * 1e-3) / 1e9 / peak,
             "roofline": roofline,
             "gpu_launches": plan.launches_per_step() * args.steps,
