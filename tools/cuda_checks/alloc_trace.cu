@@ -19,8 +19,14 @@
 //   4. each sample counts its applied moves -> bits[n]; a block scan of
 //      per-thread contiguous sample ranges gives the byte offsets off[N+1].
 // Results are identical to the oracle's heap (tests/test_gpu_parity.py).
-#include "device.cuh"
-#include "launch.h"
+#include "../../paper_2104_14129_b200/csrc/device.cuh"
+#include "../../paper_2104_14129_b200/csrc/launch.h"
+#include <cstdio>
+#include <vector>
+#include <cmath>
+#include <random>
+__device__ long long g_stamp[16];
+#define STAMP(i) if (threadIdx.x == 0) g_stamp[i] = clock64();
 
 namespace actnn {
 namespace {
@@ -105,6 +111,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
     uint64_t key_star = 0;
     long long cut = -1;
 
+    STAMP(0)
     if (any) {
         // ---- 1. min / max key
         unsigned long long lmin = ~0ull, lmax = 0ull;
@@ -130,6 +137,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             kmin = min(kmin, sh.kmin[w]);
             kmax = max(kmax, sh.kmax[w]);
         }
+        STAMP(1)
         // ---- 2. weighted radix select below the common prefix
         uint64_t prefix, pmask;
         long long rem = p.need;
@@ -194,8 +202,10 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             rem -= sh.dbefore;
             count = sh.dcount;
             hi = shift - 1;
+            if (threadIdx.x == 0) g_stamp[8]++;
             __syncthreads();  // sh.digit / dbefore / dcount are rewritten next pass
         }
+        STAMP(2)
         if (count <= 32) {
             // ---- 3a. <= 32 candidates: compact, sort by (key, index) in one warp, scan
             if (tid == 0) sh.ncand = 0;
@@ -280,10 +290,12 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
         }
     }
 
+    STAMP(3)
     // ---- 4. widths and byte offsets (thread t: a contiguous range of samples)
     const int64_t per = (p.N + kThreads - 1) / kThreads;
     const int64_t n0 = min(p.N, (int64_t)tid * per), n1 = min(p.N, n0 + per);
-    auto width = [&](int64_t n) {  // bits of sample n: its applied moves
+    long long local = 0;
+    for (int64_t n = n0; n < n1; ++n) {
         int cnt = 0;
         if (any) {
             for (int c = 0; c < M; ++c) {
@@ -292,19 +304,18 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                 if (k < key_star || (k == key_star && mv <= cut)) ++cnt;
             }
         }
-        return p.L[cnt];
-    };
-    long long local = 0;
-    for (int64_t n = n0; n < n1; ++n) local += (long long)width(n) * p.unit;
+        const int b = p.L[cnt];
+        p.bits[n] = (uint8_t)b;
+        local += (long long)b * p.unit;
+    }
     long long tot;
     long long run = block_excl_scan(local, sh, &tot);
     if (tid == 0) p.off[0] = 0;
-    for (int64_t n = n0; n < n1; ++n) {  // recomputed: no read-back of global writes
-        const int b = width(n);
-        p.bits[n] = (uint8_t)b;
-        run += (long long)b * p.unit;
+    for (int64_t n = n0; n < n1; ++n) {
+        run += (long long)p.bits[n] * p.unit;
         p.off[n + 1] = run;
     }
+    STAMP(4)
 }
 
 __global__ void uniform_bits_kernel(int64_t N, int b, int64_t unit, uint8_t* bits, int64_t* off) {
@@ -346,3 +357,29 @@ cudaError_t launch_uniform_bits(int64_t N, int b, int64_t unit, uint8_t* bits, i
 }
 
 }  // namespace actnn
+
+using namespace actnn;
+int grid_for(const void*, int, size_t, int64_t) { return 1; }
+namespace actnn { int grid_for(const void*, int, size_t, int64_t) { return 1; } }
+int main() {
+  for (int N : {256, 1024, 4096}) {
+    std::vector<double> S(N); std::mt19937 g(1); std::normal_distribution<double> nd;
+    for (auto& v : S) v = std::exp(2 * nd(g));
+    double* dS; uint8_t* db; int64_t* doff;
+    cudaMalloc(&dS, N * 8); cudaMalloc(&db, N); cudaMalloc(&doff, (N + 1) * 8);
+    cudaMemcpy(dS, S.data(), N * 8, cudaMemcpyHostToDevice);
+    AllocArgs a{}; a.sens = dS; a.gscale = nullptr; a.N = N; a.m = 4; int L[4] = {8, 4, 2, 1};
+    for (int i = 0; i < 4; ++i) a.L[i] = L[i];
+    for (int c = 0; c < 3; ++c) { double Bh = (1 << L[c]) - 1, Bl = (1 << L[c + 1]) - 1; a.freed[c] = L[c] - L[c + 1]; a.slope[c] = (1.0 / (Bl * Bl) - 1.0 / (Bh * Bh)) / a.freed[c]; }
+    a.need = 8LL * N - 2LL * N; a.unit = 98 * 32; a.bits = db; a.off = doff;
+    for (int rep = 0; rep < 3; ++rep) {
+      long long z[16] = {0}; cudaMemcpyToSymbol(g_stamp, z, sizeof(z));
+      cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+      cudaEventRecord(e0); launch_allocate(a, 0); cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      long long st[16]; cudaMemcpyFromSymbol(st, g_stamp, sizeof(st));
+      printf("N=%d event %.1f us | minmax %lld | radix %lld (passes %lld) | finish %lld | final %lld cycles\n", N, ms * 1e3, st[1] - st[0], st[2] - st[1], st[8], st[3] - st[2], st[4] - st[3]);
+    }
+  }
+  return 0;
+}
