@@ -30,6 +30,12 @@ namespace {
 #ifndef ACTNN_WS_S
 #define ACTNN_WS_S 3
 #endif
+#ifndef ACTNN_WS_PH
+#define ACTNN_WS_PH 2
+#endif
+#ifndef ACTNN_WS_LAZY
+#define ACTNN_WS_LAZY 0
+#endif
 #ifndef ACTNN_WS_MINB
 #define ACTNN_WS_MINB 2
 #endif
@@ -44,6 +50,7 @@ template <typename T>
 struct WS {
     static constexpr int U = kUnitBytes / (kG * (int)sizeof(T));  // groups per unit: 4 / 8
     static constexpr int SE = kUnitBytes / (int)sizeof(T);        // elements per stage
+    static constexpr int PH = ACTNN_WS_PH;                          // Philox chains interleaved
 };
 
 struct __align__(16) Desc {
@@ -157,6 +164,60 @@ __device__ __forceinline__ void ws_store(const float v[8], float Z, float inv14,
 // One unit: read the stage and its descriptor, release the stage, then per
 // group one Philox call and the width-specific codes/store (a warp-uniform
 // branch per group, so the Philox and data code exists once).
+template <int b>
+__device__ __forceinline__ void ws_store_any(int bw, const float v[8], float Z, float inv,
+                                             const Philox4& o, uint8_t* sg, int lane) {
+    if (bw == 2) ws_store<2>(v, Z, inv, o, sg, lane);
+    else if (bw == 1) ws_store<1>(v, Z, inv, o, sg, lane);
+    else if (bw == 4) ws_store<4>(v, Z, inv, o, sg, lane);
+    else if (bw == 8) ws_store<8>(v, Z, inv, o, sg, lane);
+    else if (bw == 3) ws_store<3>(v, Z, inv, o, sg, lane);
+    else if (bw == 5) ws_store<5>(v, Z, inv, o, sg, lane);
+    else if (bw == 6) ws_store<6>(v, Z, inv, o, sg, lane);
+    else if (bw == 7) ws_store<7>(v, Z, inv, o, sg, lane);
+}
+
+#if ACTNN_WS_LAZY
+// Lazy variant: each batch of PH groups is read from the stage just before it
+// is used, and the stage (data + descriptor) is released after the last
+// batch's reads -- only PH groups of data live in registers, which leaves room
+// for more consumer warps per SM (ACTNN_WS_MINB = 3, ACTNN_WS_S = 2).
+template <typename T>
+__device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* packed,
+                                        const RoundKeys& rk, int lane, uint64_t* empty) {
+    constexpr int U = WS<T>::U;
+    constexpr int PH = WS<T>::PH;
+    const int gcount = (int)d.gcount;
+    const int b = (int)d.b;
+    const uint64_t blk0 = d.blk0;
+    uint8_t* seg = packed + d.seg;
+#pragma unroll
+    for (int h = 0; h < U; h += PH) {
+        float v[PH][8];
+        float Z[PH], inv[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            if (h + q < gcount) lds8(st + (h + q) * kG + lane * 8, v[q]);
+            Z[q] = d.Z[h + q];
+            inv[q] = d.inv[h + q];
+        }
+        if (h + PH >= U) {  // last batch: every read of the stage is issued
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty);
+        }
+        Philox4 o[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const uint64_t blk = blk0 + (uint64_t)((h + q) * 32 + lane);
+            o[q] = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+        }
+#pragma unroll
+        for (int q = 0; q < PH; ++q)
+            if (h + q < gcount)
+                ws_store_any<0>(b, v[q], Z[q], inv[q], o[q], seg + (h + q) * 32 * b, lane);
+    }
+}
+#else
 template <typename T>
 __device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* packed,
                                         const RoundKeys& rk, int lane, uint64_t* empty) {
@@ -179,24 +240,38 @@ __device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* pac
     __syncwarp();
     if (lane == 0) mbar_arrive(empty);
     uint8_t* seg = packed + seg0;
+    // Philox draws, 4 groups at a time with no control flow between them, so
+    // the 4 ten-round dependency chains interleave (one chain alone leaves the
+    // warp waiting on IMAD.WIDE -> LOP3 latencies).  Tail units (gcount < U)
+    // draw for the absent groups too; those draws are simply not used.
+    constexpr int PH = WS<T>::PH;
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-        if (k < gcount) {
-            const float Z = Zs[k], inv = Is[k];
-            const uint64_t blk = blk0 + (uint64_t)(k * 32 + lane);
-            const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
-            uint8_t* sg = seg + k * 32 * b;
-            if (b == 2) ws_store<2>(v[k], Z, inv, o, sg, lane);
-            else if (b == 1) ws_store<1>(v[k], Z, inv, o, sg, lane);
-            else if (b == 4) ws_store<4>(v[k], Z, inv, o, sg, lane);
-            else if (b == 8) ws_store<8>(v[k], Z, inv, o, sg, lane);
-            else if (b == 3) ws_store<3>(v[k], Z, inv, o, sg, lane);
-            else if (b == 5) ws_store<5>(v[k], Z, inv, o, sg, lane);
-            else if (b == 6) ws_store<6>(v[k], Z, inv, o, sg, lane);
-            else if (b == 7) ws_store<7>(v[k], Z, inv, o, sg, lane);
+    for (int h = 0; h < U; h += PH) {
+        Philox4 o[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const uint64_t blk = blk0 + (uint64_t)((h + q) * 32 + lane);
+            o[q] = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+        }
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const int k = h + q;
+            if (k < gcount) {
+                const float Z = Zs[k], inv = Is[k];
+                uint8_t* sg = seg + k * 32 * b;
+                if (b == 2) ws_store<2>(v[k], Z, inv, o[q], sg, lane);
+                else if (b == 1) ws_store<1>(v[k], Z, inv, o[q], sg, lane);
+                else if (b == 4) ws_store<4>(v[k], Z, inv, o[q], sg, lane);
+                else if (b == 8) ws_store<8>(v[k], Z, inv, o[q], sg, lane);
+                else if (b == 3) ws_store<3>(v[k], Z, inv, o[q], sg, lane);
+                else if (b == 5) ws_store<5>(v[k], Z, inv, o[q], sg, lane);
+                else if (b == 6) ws_store<6>(v[k], Z, inv, o[q], sg, lane);
+                else if (b == 7) ws_store<7>(v[k], Z, inv, o[q], sg, lane);
+            }
         }
     }
 }
+#endif
 
 template <typename T, bool kCached>
 __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(const __grid_constant__ WSParams p) {
