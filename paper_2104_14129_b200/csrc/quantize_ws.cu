@@ -34,7 +34,7 @@ namespace {
 #define ACTNN_WS_PH 2
 #endif
 #ifndef ACTNN_WS_LAZY
-#define ACTNN_WS_LAZY 0
+#define ACTNN_WS_LAZY -1  // -1: lazy for bf16, eager for fp32 (measured best)
 #endif
 #ifndef ACTNN_WS_MINB
 #define ACTNN_WS_MINB 2
@@ -51,6 +51,7 @@ struct WS {
     static constexpr int U = kUnitBytes / (kG * (int)sizeof(T));  // groups per unit: 4 / 8
     static constexpr int SE = kUnitBytes / (int)sizeof(T);        // elements per stage
     static constexpr int PH = ACTNN_WS_PH;                          // Philox chains interleaved
+    static constexpr bool kLazy = ACTNN_WS_LAZY < 0 ? sizeof(T) == 2 : ACTNN_WS_LAZY != 0;
 };
 
 struct __align__(16) Desc {
@@ -177,13 +178,12 @@ __device__ __forceinline__ void ws_store_any(int bw, const float v[8], float Z, 
     else if (bw == 7) ws_store<7>(v, Z, inv, o, sg, lane);
 }
 
-#if ACTNN_WS_LAZY
 // Lazy variant: each batch of PH groups is read from the stage just before it
 // is used, and the stage (data + descriptor) is released after the last
 // batch's reads -- only PH groups of data live in registers, which leaves room
 // for more consumer warps per SM (ACTNN_WS_MINB = 3, ACTNN_WS_S = 2).
 template <typename T>
-__device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* packed,
+__device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t* packed,
                                         const RoundKeys& rk, int lane, uint64_t* empty) {
     constexpr int U = WS<T>::U;
     constexpr int PH = WS<T>::PH;
@@ -217,9 +217,8 @@ __device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* pac
                 ws_store_any<0>(b, v[q], Z[q], inv[q], o[q], seg + (h + q) * 32 * b, lane);
     }
 }
-#else
 template <typename T>
-__device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* packed,
+__device__ __forceinline__ void ws_unit_eager(const T* st, const Desc& d, uint8_t* packed,
                                         const RoundKeys& rk, int lane, uint64_t* empty) {
     constexpr int U = WS<T>::U;
     const int gcount = (int)d.gcount;
@@ -271,7 +270,6 @@ __device__ __forceinline__ void ws_unit(const T* st, const Desc& d, uint8_t* pac
         }
     }
 }
-#endif
 
 template <typename T, bool kCached>
 __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(const __grid_constant__ WSParams p) {
@@ -396,7 +394,10 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
         mbar_wait(&full[slot], ph);
         const Desc& d = desc[slot];
         const T* st = ring + (size_t)slot * SE;
-        ws_unit<T>(st, d, p.packed, p.rk, lane, &empty[slot]);
+        if constexpr (WS<T>::kLazy)
+            ws_unit_lazy<T>(st, d, p.packed, p.rk, lane, &empty[slot]);
+        else
+            ws_unit_eager<T>(st, d, p.packed, p.rk, lane, &empty[slot]);
         if (++s == kS) {
             s = 0;
             ph ^= 1u;

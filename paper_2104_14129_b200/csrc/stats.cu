@@ -18,8 +18,13 @@
 namespace actnn {
 namespace {
 
-constexpr int kBlock = 256;
-constexpr int kU = 4;
+// groups per warp per chunk: 4 (fp32: 4 KB in flight per warp) or 8 (bf16:
+// also 4 KB); a CTA has 32 / U warps so that a chunk is 32 groups.
+template <typename T>
+struct SCfg {
+    static constexpr int U = 4;  // (8 for bf16 measured slower: 96 regs, 20 warps/SM)
+    static constexpr int Block = (kChunk / U) * 32;
+};
 constexpr unsigned kFull = 0xffffffffu;
 
 struct SParams {
@@ -33,7 +38,9 @@ struct SParams {
 };
 
 template <typename T, bool kFast>
-__global__ void __launch_bounds__(kBlock) group_stats_kernel(SParams p) {
+__global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) {
+    constexpr int kU = SCfg<T>::U;
+    constexpr int kBlock = SCfg<T>::Block;
     __shared__ float sZ[kChunk], sM[kChunk];
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
@@ -135,11 +142,11 @@ cudaError_t run(const StatsArgs& a, cudaStream_t s) {
               reinterpret_cast<unsigned int*>(a.T + a.N * a.nch)};
     const int64_t tiles = a.N * a.nch;
     if (a.fast) {
-        const int grid = grid_for((const void*)group_stats_kernel<T, true>, kBlock, 0, tiles);
-        group_stats_kernel<T, true><<<grid, kBlock, 0, s>>>(p);
+        const int grid = grid_for((const void*)group_stats_kernel<T, true>, SCfg<T>::Block, 0, tiles);
+        group_stats_kernel<T, true><<<grid, SCfg<T>::Block, 0, s>>>(p);
     } else {
-        const int grid = grid_for((const void*)group_stats_kernel<T, false>, kBlock, 0, tiles);
-        group_stats_kernel<T, false><<<grid, kBlock, 0, s>>>(p);
+        const int grid = grid_for((const void*)group_stats_kernel<T, false>, SCfg<T>::Block, 0, tiles);
+        group_stats_kernel<T, false><<<grid, SCfg<T>::Block, 0, s>>>(p);
     }
     return cudaGetLastError();
 }
