@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
+                    help="replay the step from a captured CUDA graph (default at N=1)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     return ap.parse_args()
 
 
@@ -207,6 +210,7 @@ def config_dict(wl, args, world, n_loc):
         "parallelism": f"dp{world} (batch-sharded; all-gather of S per tensor)" if world > 1
         else "dp1",
         "l2": "inputs larger than L2: %.1f GB per step per GPU vs 126 MB L2" % (E * s_in / 1e9),
+        "cuda_graph": bool(getattr(args, "graph", False)),
     }
 
 
@@ -313,8 +317,9 @@ def main():
     max_numel = max(x.numel() for x in xs)
     outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(2)]
     out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
-    stream = torch.cuda.current_stream(dev)
-    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
+    stream = torch.cuda.Stream(dev)   # main stream (non-default so it can be captured)
+    torch.cuda.set_stream(stream)
+    sp =__import__("ctypes").c_void_p(stream.cuda_stream)
     nl = len(plan.layers)
 
     side = torch.cuda.Stream(dev)                 # stats chain
@@ -352,6 +357,28 @@ def main():
     for _ in range(max(3, args.warmup)):
         step()
     barrier()
+
+    # ---- optional: capture the whole pipelined step in one CUDA graph (removes
+    # the ~430 per-step CPU launches; every kernel still runs on every replay)
+    # Seeds are per tensor and fixed across steps in both modes, so a replay does
+    # exactly the work of an eager step.  At N>1 the step holds a collective
+    # (all-gather of S); it stays eager there.
+    graph = None
+    if args.graph is None:
+        args.graph = world == 1
+    if args.graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            plan.compress_all(stream, side, alloc_s)
+            plan.decompress_all(outs, out_dt, [stream, aux])
+        graph.replay()
+        barrier()
+        eager_step = step
+
+        def step(ev=None):  # noqa: F811
+            if ev is not None or flags["phases"]:
+                return eager_step(ev)
+            graph.replay()
 
     # ---- headline: K steps, one event pair, max over ranks
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

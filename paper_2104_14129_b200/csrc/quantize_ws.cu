@@ -18,6 +18,8 @@
 // per group, fixed-point SR codes, packing and word stores.  Moving the unit
 // walk, the divisions and the metadata traffic to one warp amortises them over
 // kCons * U groups per producer step instead of U per consumer step.
+#include <cstdlib>
+
 #include "device.cuh"
 #include "launch.h"
 
@@ -420,7 +422,16 @@ void launch_ws(WSParams p, int64_t units, cudaStream_t s) {
                              (int)ws_smem_bytes<T>());
         attr = true;
     }
-    const int grid = grid_for(k, kThreads, ws_smem_bytes<T>(), (units + kCons - 1) / kCons);
+    int grid = grid_for(k, kThreads, ws_smem_bytes<T>(), (units + kCons - 1) / kCons);
+    // ACTNN_WS_CTAS_PER_SM caps the persistent grid (tuning: leaves room on every
+    // SM for a concurrently running stats kernel of the next tensor)
+    if (const char* e = std::getenv("ACTNN_WS_CTAS_PER_SM")) {
+        int sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int cap = sms * std::atoi(e);
+        if (cap > 0 && grid > cap) grid = cap;
+    }
     const uint32_t nwarps = (uint32_t)grid * kCons;
     p.step_n = nwarps / p.nb;
     p.step_j = nwarps % p.nb;
