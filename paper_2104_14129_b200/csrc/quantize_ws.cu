@@ -99,6 +99,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// hi32(a * b) + c in one IMAD.HI
+__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// Codes of one lane's 8 elements at b <= 2, two elements per 32-bit register:
+// t = RN(d * inv14 + 1.5 2^23) holds q = RNE(d * inv14) < 2^16 in its low half
+// (the magic's low 16 bits are zero), so one byte permute gives
+// T = q_y << 16 | q_x; adding the two 14-bit draws (w & 0x3FFF3FFF) cannot
+// carry across halves (q + r < (B + 1) 2^14 <= 2^16), and bits 14.. of each
+// half are the codes (ACTNN-Q v1 O5-O7).  One multiply-high per pair moves the
+// two codes to their packed positions; the positions of different pairs are
+// disjoint, so the accumulation is an add.
 template <int b>
 __device__ __forceinline__ uint32_t ws_codes_small(const float v[8], float Z, float inv14,
                                                    const Philox4& o) {
@@ -111,12 +126,12 @@ __device__ __forceinline__ uint32_t ws_codes_small(const float v[8], float Z, fl
     for (int p = 0; p < 4; ++p) {
         const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
         const float2 t = __ffma2_rn(d, iv, mg);
-        uint32_t T = __float_as_uint(t.y) * 65536u + __float_as_uint(t.x);
-        T = T + (w[p] & 0x3FFF3FFFu) - 0x4B400000u;
+        uint32_t T = __byte_perm(__float_as_uint(t.x), __float_as_uint(t.y), 0x5410);
+        T += w[p] & 0x3FFF3FFFu;
         if (b == 2)
-            acc |= __umulhi(T & 0xC000C000u, (1u << (18 + 4 * p)) + (1u << (4 + 4 * p)));
+            acc = madhi(T & 0xC000C000u, (1u << (18 + 4 * p)) + (1u << (4 + 4 * p)), acc);
         else
-            acc |= __umulhi(T & 0x40004000u, (1u << (18 + 2 * p)) + (1u << (3 + 2 * p)));
+            acc = madhi(T & 0x40004000u, (1u << (18 + 2 * p)) + (1u << (3 + 2 * p)), acc);
     }
     return acc & ((1u << (8 * b)) - 1u);
 }
@@ -184,6 +199,38 @@ __device__ __forceinline__ void ws_store_any(int bw, const float v[8], float Z, 
 // is used, and the stage (data + descriptor) is released after the last
 // batch's reads -- only PH groups of data live in registers, which leaves room
 // for more consumer warps per SM (ACTNN_WS_MINB = 3, ACTNN_WS_S = 2).
+template <int b, typename T>
+__device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_t blk,
+                                             uint8_t* seg, const RoundKeys& rk, int lane,
+                                             uint64_t* empty) {
+    constexpr int U = WS<T>::U;
+    constexpr int PH = WS<T>::PH;
+#pragma unroll
+    for (int h = 0; h < U; h += PH) {
+        float v[PH][8];
+        float Z[PH], inv[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            lds8(st + (h + q) * kG + lane * 8, v[q]);
+            Z[q] = d.Z[h + q];
+            inv[q] = d.inv[h + q];
+        }
+        if (h + PH >= U) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty);
+        }
+        Philox4 o[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const uint64_t c = blk + (uint64_t)((h + q) * 32);
+            o[q] = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), rk);
+        }
+#pragma unroll
+        for (int q = 0; q < PH; ++q)
+            ws_store<b>(v[q], Z[q], inv[q], o[q], seg + (h + q) * 32 * b, lane);
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t* packed,
                                         const RoundKeys& rk, int lane, uint64_t* empty) {
@@ -193,6 +240,13 @@ __device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t
     const int b = (int)d.b;
     const uint64_t blk0 = d.blk0;
     uint8_t* seg = packed + d.seg;
+    if (gcount == U) {  // the common case, at the allocator's widths {1, 2, 4, 8}
+        const uint64_t blk = blk0 + (uint64_t)lane;
+        if (b == 2) return ws_lazy_full<2, T>(st, d, blk, seg, rk, lane, empty);
+        if (b == 1) return ws_lazy_full<1, T>(st, d, blk, seg, rk, lane, empty);
+        if (b == 4) return ws_lazy_full<4, T>(st, d, blk, seg, rk, lane, empty);
+        if (b == 8) return ws_lazy_full<8, T>(st, d, blk, seg, rk, lane, empty);
+    }
 #pragma unroll
     for (int h = 0; h < U; h += PH) {
         float v[PH][8];
@@ -219,6 +273,26 @@ __device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t
                 ws_store_any<0>(b, v[q], Z[q], inv[q], o[q], seg + (h + q) * 32 * b, lane);
     }
 }
+// A full unit (gcount == U) at a width fixed at compile time: the Philox draws
+// and the codes of all U groups straight-line, no per-group dispatch.
+template <int b, int U, int PH>
+__device__ __forceinline__ void ws_full_unit(const float (&v)[U][8], const float (&Zs)[U],
+                                             const float (&Is)[U], uint64_t blk, uint8_t* seg,
+                                             const RoundKeys& rk, int lane) {
+#pragma unroll
+    for (int h = 0; h < U; h += PH) {
+        Philox4 o[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const uint64_t c = blk + (uint64_t)((h + q) * 32);
+            o[q] = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), rk);
+        }
+#pragma unroll
+        for (int q = 0; q < PH; ++q)
+            ws_store<b>(v[h + q], Zs[h + q], Is[h + q], o[q], seg + (h + q) * 32 * b, lane);
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void ws_unit_eager(const T* st, const Desc& d, uint8_t* packed,
                                         const RoundKeys& rk, int lane, uint64_t* empty) {
@@ -241,6 +315,14 @@ __device__ __forceinline__ void ws_unit_eager(const T* st, const Desc& d, uint8_
     __syncwarp();
     if (lane == 0) mbar_arrive(empty);
     uint8_t* seg = packed + seg0;
+    if (gcount == U) {  // the common case, at the allocator's widths {1, 2, 4, 8}
+        constexpr int PH = WS<T>::PH;
+        const uint64_t blk = blk0 + (uint64_t)lane;
+        if (b == 2) return ws_full_unit<2, U, PH>(v, Zs, Is, blk, seg, rk, lane);
+        if (b == 1) return ws_full_unit<1, U, PH>(v, Zs, Is, blk, seg, rk, lane);
+        if (b == 4) return ws_full_unit<4, U, PH>(v, Zs, Is, blk, seg, rk, lane);
+        if (b == 8) return ws_full_unit<8, U, PH>(v, Zs, Is, blk, seg, rk, lane);
+    }
     // Philox draws, 4 groups at a time with no control flow between them, so
     // the 4 ten-round dependency chains interleave (one chain alone leaves the
     // warp waiting on IMAD.WIDE -> LOP3 latencies).  Tail units (gcount < U)
