@@ -455,7 +455,8 @@ def main():
     launches_dom = nl
     ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": {"stats": "group_stats_kernel (K1)",
-                                           "quantize": "quantize_fast_kernel (K3)",
+                                           "quantize": "quantize_ws_kernel (K3)" if plan.mixed
+                                           else "quantize_fast_kernel (K3)",
                                            "dequantize": "dequantize_fast_kernel (K4)"}[dom],
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "peak_source": peak_src, "traffic": ncu_traffic(dom),

@@ -38,12 +38,16 @@ namespace {
 #ifndef ACTNN_WS_LAZY
 #define ACTNN_WS_LAZY -1  // -1: lazy for bf16, eager for fp32 (measured best)
 #endif
+#ifndef ACTNN_WS_MD
+#define ACTNN_WS_MD 1  // rounds of (gmin, gmax) prefetched by the producer (1-6 measured: 1 best)
+#endif
 #ifndef ACTNN_WS_MINB
 #define ACTNN_WS_MINB 2
 #endif
 constexpr int kCons = ACTNN_WS_CONS;      // consumer warps per CTA
 constexpr int kThreads = (kCons + 1) * 32;
 constexpr int kS = ACTNN_WS_S;            // stages per consumer
+constexpr int kMD = ACTNN_WS_MD;
 constexpr int kUnitBytes = 4096;          // one TMA copy per unit
 constexpr int kNCap = 2048;
 constexpr unsigned kFull = 0xffffffffu;
@@ -407,11 +411,29 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
                 mx[t] = k < gcount ? __ldg(p.gmax + g + k) : 0.0f;
             }
         };
-        float cmn[GPL], cmx[GPL];
-        if (n < p.N) load_meta(n, j, cmn, cmx);
-        for (uint32_t r = 0;; ++r) {
+        auto advance = [&](uint32_t& n_, uint32_t& j_) {
+            n_ += p.step_n;
+            j_ += p.step_j;
+            if (j_ >= p.nb) {
+                j_ -= p.nb;
+                ++n_;
+            }
+        };
+        // (gmin, gmax) are prefetched kMD rounds ahead into a register ring
+        // indexed by the unrolled round counter (no moves of pending loads):
+        // one round ahead leaves the producer waiting out the loaded HBM
+        // latency every round.
+        float qmn[kMD][GPL], qmx[kMD][GPL];
+        uint32_t pn = n, pj = j;
+#pragma unroll
+        for (int i = 0; i < kMD; ++i) {
+            if (pn < p.N) load_meta(pn, pj, qmn[i], qmx[i]);
+            advance(pn, pj);
+        }
+        // one round: returns false once no lane has work left
+        auto round = [&](uint32_t r, float (&cmn)[GPL], float (&cmx)[GPL]) -> bool {
             const bool valid = n < p.N;
-            if (!__any_sync(kFull, valid)) break;
+            if (!__any_sync(kFull, valid)) return false;
             const int s = (int)(r % kS);
             const int slot = c * kS + s;
             if (r >= (uint32_t)kS && valid && kl == 0)
@@ -425,13 +447,6 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
                 bulk_g2s(ring + (size_t)slot * SE, x + (uint64_t)n * p.D + (uint64_t)gi * kG, bytes,
                          &full[slot]);
             }
-            uint32_t nn = n + p.step_n, nj = j + p.step_j;
-            if (nj >= p.nb) {
-                nj -= p.nb;
-                ++nn;
-            }
-            float nmn[GPL], nmx[GPL];
-            if (nn < p.N) load_meta(nn, nj, nmn, nmx);
             if (valid) {
                 const int b = kCached ? (int)s_bits[n] : (int)p.bits[n];
                 const uint32_t g = n * p.ng + gi;
@@ -457,13 +472,18 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
             }
             __syncwarp();  // descriptor writes of the consumer's lanes precede the arrive
             if (valid && kl == 0) mbar_arrive(&full[slot]);
-            n = nn;
-            j = nj;
+            // this ring entry is consumed: refill it with round r + kMD
+            if (pn < p.N) load_meta(pn, pj, cmn, cmx);
+            advance(pn, pj);
+            advance(n, j);
+            return true;
+        };
+        for (uint32_t r = 0;; r += kMD) {
+            bool more = true;
 #pragma unroll
-            for (int t = 0; t < GPL; ++t) {
-                cmn[t] = nmn[t];
-                cmx[t] = nmx[t];
-            }
+            for (int i = 0; i < kMD; ++i)
+                if (more) more = round(r + i, qmn[i], qmx[i]);
+            if (!more) break;
         }
         return;
     }
