@@ -57,10 +57,11 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel_key):
+def ncu_traffic(kernel_key, mixed=True):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel, from
     the committed ncu launch list of one C3 step (profiles/traffic.json)."""
-    name = {"stats": "group_stats_kernel", "quantize": "quantize_fast_kernel",
+    name = {"stats": "group_stats_kernel",
+            "quantize": "quantize_ws_kernel" if mixed else "quantize_fast_kernel",
             "dequantize": "dequantize_fast_kernel"}[kernel_key]
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -459,7 +460,7 @@ def main():
                                            else "quantize_fast_kernel (K3)",
                                            "dequantize": "dequantize_fast_kernel (K4)"}[dom],
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "peak_source": peak_src, "traffic": ncu_traffic(dom),
+                "peak_source": peak_src, "traffic": ncu_traffic(dom, plan.mixed) if wl.name == "c3" else None,
                 "algorithmic_bytes_per_launch": alg[dom] / launches_dom,
                 "avg_launch_us": kt[dom] * 1e3 / launches_dom,
                 "per_kernel": {k: {"ms_per_step": kt[k], "share_of_step": kt[k] / ms_step,
