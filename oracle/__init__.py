@@ -65,6 +65,12 @@ def _load():
                                                  ctypes.c_int]),
             "oracle_dequantize_group": (None, [P, I32, I32, ctypes.c_float, ctypes.c_float,
                                                P, P]),
+            "oracle_meta_bf16": (U32, [ctypes.c_float, ctypes.c_float]),
+            "oracle_quantize_group_bf16meta": (ctypes.c_int, [P, I32, I32, I32, U64, U64, P, P]),
+            "oracle_quantize_bf16meta": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I32, P, U64,
+                                                        I64, P, P, ctypes.c_int]),
+            "oracle_dequantize_bf16meta": (ctypes.c_int, [P, P, P, I64, I64, I32, P,
+                                                          ctypes.c_int, ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -219,6 +225,67 @@ def dequantize_group(seg, length: int, b: int, zmin: float, scale: float):
     _load().oracle_dequantize_group(_ptr(seg), length, b, float(zmin), float(scale),
                                     _ptr(codes), _ptr(out))
     return codes, out
+
+
+# ---------------------------------------------------------------- NEXT-1
+# bf16 metadata (DESIGN reading 21): one uint32 word
+# per group, low half = Z' (bf16 toward -inf of Z), high half = R' (bf16
+# toward +inf of RU32(M - Z')); quantisation and dequantisation use float(Z'),
+# float(R').
+
+def meta_bf16(Z: float, M: float) -> int:
+    """The group's metadata word from its canonical min Z and max M."""
+    return int(_load().oracle_meta_bf16(float(np.float32(Z)), float(np.float32(M))))
+
+
+def meta_fields(meta) -> tuple:
+    """Split words into (Z', R') as float32 arrays (exact widening)."""
+    w = np.ascontiguousarray(meta, np.uint32)
+    Z = (w << np.uint32(16)).view(np.float32)
+    R = (w & np.uint32(0xFFFF0000)).view(np.float32)
+    return Z, R
+
+
+def quantize_group_bf16meta(h: np.ndarray, b: int, seed: int, e0: int, G: int = 256):
+    """One group -> (segment bytes [G*b/8], metadata word)."""
+    h = np.ascontiguousarray(h, np.float32)
+    seg = np.zeros(G * b // 8, np.uint8)
+    m = ctypes.c_uint32()
+    st = _load().oracle_quantize_group_bf16meta(_ptr(h), len(h), G, b, seed, e0, _ptr(seg),
+                                                ctypes.byref(m))
+    if st != 0:
+        raise ValueError(f"oracle_quantize_group_bf16meta failed: {st}")
+    return seg, int(m.value)
+
+
+def quantize_bf16meta(x: np.ndarray, bits, seed: int, sample_base: int = 0, G: int = 256,
+                      threads: int = 1):
+    """x [N, D] -> (packed u8 [off[N]], meta u32 [N, ng], off [N+1])."""
+    x, dt = _as_x(x)
+    N, D = x.shape
+    bits = np.ascontiguousarray(np.broadcast_to(np.asarray(bits, np.uint8), (N,)))
+    off = offsets(bits, D, G)
+    ng = ceil_div(D, G)
+    packed = np.zeros(int(off[-1]), np.uint8)
+    meta = np.zeros((N, ng), np.uint32)
+    st = _load().oracle_quantize_bf16meta(_ptr(x), dt, N, D, G, _ptr(bits), seed, sample_base,
+                                          _ptr(packed), _ptr(meta), threads)
+    if st != 0:
+        raise ValueError(f"oracle_quantize_bf16meta failed: {st}")
+    return packed, meta, off
+
+
+def dequantize_bf16meta(packed, meta, bits, N: int, D: int, G: int = 256,
+                        out_dtype: int = F32, threads: int = 1) -> np.ndarray:
+    bits = np.ascontiguousarray(np.broadcast_to(np.asarray(bits, np.uint8), (N,)))
+    packed = np.ascontiguousarray(packed, np.uint8)
+    meta = np.ascontiguousarray(meta, np.uint32)
+    out = np.zeros((N, D), np.float32 if out_dtype == F32 else np.uint16)
+    st = _load().oracle_dequantize_bf16meta(_ptr(packed), _ptr(meta), _ptr(bits), N, D, G,
+                                            _ptr(out), out_dtype, threads)
+    if st != 0:
+        raise ValueError(f"oracle_dequantize_bf16meta failed: {st}")
+    return out
 
 
 def sharded_quantize(x: np.ndarray, k: int, avg_bits: float, seed: int,

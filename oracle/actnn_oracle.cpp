@@ -278,24 +278,18 @@ extern "C" void oracle_offsets(const uint8_t* bits, int64_t N, int64_t D, int32_
     for (int64_t n = 0; n < N; ++n) off[n + 1] = off[n] + (int64_t)bits[n] * ng * G / 8;
 }
 
-/* O3-O9 for one group, in the paper's order:
- *   Z = min, R = max - min                           (O3)
- *   u_bar = B (h - Z) / R as the 14-bit fixed point  (O4-O5)
- *       q = RNE(RN(h - Z) * RN(B / R) * 2^14)
+/* O4-O8 for one group whose zero point Z and range R are given:
+ *   scale = RN(R / B); u_bar = B (h - Z) / R as the 14-bit fixed point
+ *       q = RNE(RN(h - Z) * RN(B / R) * 2^14)                      (O4-O5)
  *   u_hat = ceil(u_bar) w.p. frac(u_bar) else floor   (O6-O7)
  *       code = (q + r) >> 14 with r uniform in [0, 2^14)
  *   codes LSB-first into a bit stream                (O8)
- */
-extern "C" int oracle_quantize_group(const float* h, int32_t len, int32_t G, int32_t b,
-                                     uint64_t seed, uint64_t e0, uint8_t* seg, float* zmin,
-                                     float* scale) {
-    float Z, M;
-    group_min_max(h, len, &Z, &M);
-    float R = M - Z;
+ * Returns the scale, or NaN if the q <= B*2^14 invariant fails. */
+static float sr_pack_group(const float* h, int32_t len, int32_t G, int32_t b, uint64_t seed,
+                           uint64_t e0, float Z, float R, uint8_t* seg) {
     uint32_t B = (1u << b) - 1u;
     float Bf = (float)B;
-    *zmin = Z;
-    *scale = R / Bf;
+    float scale = R / Bf;
     /* degenerate group (DESIGN reading 16): every code 0, dequantises to Z */
     float inv14 = (R < 0x1p-96f) ? 0.0f : (Bf / R) * 16384.0f;
     std::memset(seg, 0, (size_t)G * (size_t)b / 8);
@@ -304,7 +298,7 @@ extern "C" int oracle_quantize_group(const float* h, int32_t len, int32_t G, int
         /* 24b x 24b product is exact in binary64; nearbyint is RNE */
         double qd = std::nearbyint((double)delta * (double)inv14);
         uint64_t q = (uint64_t)qd;
-        if (q > ((uint64_t)B << 14)) return ORACLE_ERR_INVARIANT;
+        if (q > ((uint64_t)B << 14)) return NAN;
         uint64_t r = oracle_random14(seed, e0 + (uint64_t)k);
         uint32_t code = (uint32_t)((q + r) >> 14);
         for (int32_t t = 0; t < b; ++t) {
@@ -312,13 +306,94 @@ extern "C" int oracle_quantize_group(const float* h, int32_t len, int32_t G, int
             if ((code >> t) & 1u) seg[bit >> 3] |= (uint8_t)(1u << (bit & 7));
         }
     }
+    return scale;
+}
+
+/* O3-O9 for one group, in the paper's order: Z = min,
+ * R = RN(max - min) (O3), then O4-O8 above. */
+extern "C" int oracle_quantize_group(const float* h, int32_t len, int32_t G, int32_t b,
+                                     uint64_t seed, uint64_t e0, uint8_t* seg, float* zmin,
+                                     float* scale) {
+    float Z, M;
+    group_min_max(h, len, &Z, &M);
+    float R = M - Z;
+    *zmin = Z;
+    float s = sr_pack_group(h, len, G, b, seed, e0, Z, R, seg);
+    if (std::isnan(s)) return ORACLE_ERR_INVARIANT;
+    *scale = s;
     return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-1: bf16 metadata ("store the per-group range and zero points in  */
+/* bfloat16, so each group costs extra 32 bits"; "R and Z ... */
+/* rounded to bfloat16 BEFORE scaling (stored and used values identical)").    */
+/* DESIGN reading 21: outward rounding, so [Z', Z' + R'] contains the group:   */
+/*   Z' = bf16 rounded toward -inf of Z                                         */
+/*   R' = bf16 rounded toward +inf of RU32(M - Z')  (>= the exact M - Z')       */
+/* then O4-O10 run with (Z, R) := (float(Z'), float(R')).                       */
+/* ------------------------------------------------------------------------- */
+static uint32_t f2u(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return u;
+}
+static float u2f(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+/* bf16 toward -inf / toward +inf of a finite fp32 value (bf16 = high 16 bits;
+ * the bit pattern of same-signed floats is monotone in magnitude). */
+static uint16_t bf16_down(float f) {
+    uint32_t u = f2u(f);
+    uint32_t hi = u >> 16;
+    if ((u & 0xFFFFu) && (u >> 31)) hi += 1; /* negative: away from zero */
+    return (uint16_t)hi;
+}
+static uint16_t bf16_up(float f) {
+    uint32_t u = f2u(f);
+    uint32_t hi = u >> 16;
+    if ((u & 0xFFFFu) && !(u >> 31)) hi += 1; /* positive: away from zero */
+    return (uint16_t)hi;
+}
+
+/* RU(a - b) in fp32: RN difference plus Knuth's exact TwoSum error term. */
+static float sub_round_up(float a, float b) {
+    float nb = -b;
+    float s = a + nb;
+    float bv = s - a;
+    float av = s - bv;
+    float err = (a - av) + (nb - bv);
+    if (err > 0.0f) s = std::nextafterf(s, INFINITY);
+    return s;
+}
+
+extern "C" uint32_t oracle_meta_bf16(float Z, float M) {
+    uint16_t zb = bf16_down(Z);
+    float Zp = u2f((uint32_t)zb << 16);
+    uint16_t rb = bf16_up(sub_round_up(M, Zp));
+    return (uint32_t)zb | ((uint32_t)rb << 16);
+}
+
+extern "C" int oracle_quantize_group_bf16meta(const float* h, int32_t len, int32_t G, int32_t b,
+                                              uint64_t seed, uint64_t e0, uint8_t* seg,
+                                              uint32_t* meta) {
+    float Z, M;
+    group_min_max(h, len, &Z, &M);
+    uint32_t w = oracle_meta_bf16(Z, M);
+    *meta = w;
+    float Zs = u2f(w << 16), Rs = u2f(w & 0xFFFF0000u);
+    float s = sr_pack_group(h, len, G, b, seed, e0, Zs, Rs, seg);
+    return std::isnan(s) ? ORACLE_ERR_INVARIANT : ORACLE_OK;
 }
 
 /* Samples [n0, n1) of a tensor; shared by the thread fan-out below. */
 static int quantize_range(const void* x, int dtype, int64_t n0, int64_t n1, int64_t D,
                           int32_t G, const uint8_t* bits, const int64_t* off, uint64_t seed,
-                          int64_t sample_base, uint8_t* packed, float* zmin, float* scale) {
+                          int64_t sample_base, uint8_t* packed, float* zmin, float* scale,
+                          uint32_t* meta) {
     int64_t ng = ceil_div(D, G);
     std::vector<float> h(G);
     for (int64_t n = n0; n < n1; ++n) {
@@ -328,8 +403,10 @@ static int quantize_range(const void* x, int dtype, int64_t n0, int64_t n1, int6
             for (int32_t k = 0; k < len; ++k) h[k] = widen(x, dtype, n * D + i * G + k);
             uint64_t e0 = (uint64_t)(sample_base + n) * (uint64_t)D + (uint64_t)(i * G);
             uint8_t* seg = packed + off[n] + i * (int64_t)G * b / 8;
-            int st = oracle_quantize_group(h.data(), len, G, b, seed, e0, seg,
-                                           &zmin[n * ng + i], &scale[n * ng + i]);
+            int st = meta ? oracle_quantize_group_bf16meta(h.data(), len, G, b, seed, e0, seg,
+                                                           &meta[n * ng + i])
+                          : oracle_quantize_group(h.data(), len, G, b, seed, e0, seg,
+                                                  &zmin[n * ng + i], &scale[n * ng + i]);
             if (st != ORACLE_OK) return st;
         }
     }
@@ -367,7 +444,21 @@ extern "C" int oracle_quantize(const void* x, int dtype, int64_t N, int64_t D, i
     oracle_offsets(bits, N, D, G, off.data());
     return fan_out(N, threads, [&](int64_t n0, int64_t n1) {
         return quantize_range(x, dtype, n0, n1, D, G, bits, off.data(), seed, sample_base,
-                              packed, zmin, scale);
+                              packed, zmin, scale, nullptr);
+    });
+}
+
+extern "C" int oracle_quantize_bf16meta(const void* x, int dtype, int64_t N, int64_t D,
+                                        int32_t G, const uint8_t* bits, uint64_t seed,
+                                        int64_t sample_base, uint8_t* packed, uint32_t* meta,
+                                        int threads) {
+    if (N < 0 || D < 0 || G < 8 || G % 8 || sample_base < 0) return ORACLE_ERR_INVALID;
+    if (!bits_ok(bits, N)) return ORACLE_ERR_INVALID;
+    std::vector<int64_t> off((size_t)N + 1);
+    oracle_offsets(bits, N, D, G, off.data());
+    return fan_out(N, threads, [&](int64_t n0, int64_t n1) {
+        return quantize_range(x, dtype, n0, n1, D, G, bits, off.data(), seed, sample_base,
+                              packed, nullptr, nullptr, meta);
     });
 }
 
@@ -386,9 +477,11 @@ extern "C" void oracle_dequantize_group(const uint8_t* seg, int32_t len, int32_t
     }
 }
 
-extern "C" int oracle_dequantize(const uint8_t* packed, const float* zmin, const float* scale,
-                                 const uint8_t* bits, int64_t N, int64_t D, int32_t G,
-                                 void* out, int out_dtype, int threads) {
+/* [N, D] tensor: per group (Z, scale) from fp32 arrays (v1) or from the bf16
+ * word (NEXT-1: Z = float(Z'), scale = RN(float(R') / B)). */
+static int dequantize_all(const uint8_t* packed, const float* zmin, const float* scale,
+                          const uint32_t* meta, const uint8_t* bits, int64_t N, int64_t D,
+                          int32_t G, void* out, int out_dtype, int threads) {
     if (N < 0 || D < 0 || G < 8 || G % 8) return ORACLE_ERR_INVALID;
     if (!bits_ok(bits, N)) return ORACLE_ERR_INVALID;
     int64_t ng = ceil_div(D, G);
@@ -401,8 +494,16 @@ extern "C" int oracle_dequantize(const uint8_t* packed, const float* zmin, const
             for (int64_t i = 0; i < ng; ++i) {
                 int32_t len = (int32_t)std::min<int64_t>(G, D - i * G);
                 const uint8_t* seg = packed + off[n] + i * (int64_t)G * b / 8;
-                oracle_dequantize_group(seg, len, b, zmin[n * ng + i], scale[n * ng + i],
-                                        nullptr, v.data());
+                float Z, s;
+                if (meta) {
+                    uint32_t w = meta[n * ng + i];
+                    Z = u2f(w << 16);
+                    s = u2f(w & 0xFFFF0000u) / (float)((1u << b) - 1u);
+                } else {
+                    Z = zmin[n * ng + i];
+                    s = scale[n * ng + i];
+                }
+                oracle_dequantize_group(seg, len, b, Z, s, nullptr, v.data());
                 for (int32_t k = 0; k < len; ++k) {
                     int64_t idx = n * D + i * G + k;
                     if (out_dtype == ORACLE_F32)
@@ -414,4 +515,17 @@ extern "C" int oracle_dequantize(const uint8_t* packed, const float* zmin, const
         }
         return ORACLE_OK;
     });
+}
+
+extern "C" int oracle_dequantize(const uint8_t* packed, const float* zmin, const float* scale,
+                                 const uint8_t* bits, int64_t N, int64_t D, int32_t G,
+                                 void* out, int out_dtype, int threads) {
+    return dequantize_all(packed, zmin, scale, nullptr, bits, N, D, G, out, out_dtype, threads);
+}
+
+extern "C" int oracle_dequantize_bf16meta(const uint8_t* packed, const uint32_t* meta,
+                                          const uint8_t* bits, int64_t N, int64_t D, int32_t G,
+                                          void* out, int out_dtype, int threads) {
+    return dequantize_all(packed, nullptr, nullptr, meta, bits, N, D, G, out, out_dtype,
+                          threads);
 }

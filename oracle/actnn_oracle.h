@@ -87,6 +87,23 @@ int oracle_dequantize(const uint8_t* packed, const float* zmin, const float* sca
                       const uint8_t* bits, int64_t N, int64_t D, int32_t G,
                       void* out, int out_dtype, int threads);
 
+/* NEXT-1, bf16 metadata ("store the per-group range and zero points in
+ * bfloat16, so each group costs extra 32 bits"; DESIGN
+ * reading 21).  One 32-bit word per group: bits 0-15 = Z' = bf16 of Z rounded
+ * toward -inf, bits 16-31 = R' = bf16 of RU32(M - Z') rounded toward +inf, so
+ * [Z', Z' + R'] contains every element of the group.  Quantisation and
+ * dequantisation use the stored values: O4-O10 with Z := float(Z'),
+ * R := float(R'), scale = RN(R / B). */
+uint32_t oracle_meta_bf16(float Z, float M);
+int oracle_quantize_group_bf16meta(const float* h, int32_t len, int32_t G, int32_t b,
+                                   uint64_t seed, uint64_t e0, uint8_t* seg, uint32_t* meta);
+int oracle_quantize_bf16meta(const void* x, int dtype, int64_t N, int64_t D, int32_t G,
+                             const uint8_t* bits, uint64_t seed, int64_t sample_base,
+                             uint8_t* packed, uint32_t* meta, int threads);
+int oracle_dequantize_bf16meta(const uint8_t* packed, const uint32_t* meta,
+                               const uint8_t* bits, int64_t N, int64_t D, int32_t G,
+                               void* out, int out_dtype, int threads);
+
 /* O10 for one group: codes from a segment and dequantised fp32 values. */
 void oracle_dequantize_group(const uint8_t* seg, int32_t len, int32_t b, float zmin,
                              float scale, uint32_t* codes, float* out);
