@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="actnn", choices=["actnn", "reference"])
     ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--meta", default="f32", choices=["f32", "bf16"],
+                    help="per-group metadata: fp32 (zmin, scale) or the paper's bf16 words")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -123,17 +125,19 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ helpers
-def algorithmic_bytes(layers, bits_host, s_in, s_out, mixed):
-    """Per-kernel algorithmic bytes (SURVEY §8(d) / DESIGN.md 'Roofline')."""
+def algorithmic_bytes(layers, bits_host, s_in, s_out, mixed, meta_bytes=8):
+    """Per-kernel algorithmic bytes (SURVEY §8(d) / DESIGN.md 'Roofline').
+    meta_bytes: stored metadata per group (8 fp32, 4 with bf16 words)."""
     tot = {"stats": 0, "quantize": 0, "dequantize": 0}
     for L, b in zip(layers, bits_host):
         groups = L.N * L.ng
         E = L.N * L.D
         packed = int(b.long().sum()) * L.ng * 32
-        meta = 8 * groups
+        mm = 8 * groups           # gmin/gmax (K1 -> K3), always fp32
+        meta = meta_bytes * groups
         if mixed:
-            tot["stats"] += E * s_in + meta + 8 * L.N * (-(-L.ng // 32))
-            tot["quantize"] += E * s_in + meta + packed + meta + 9 * L.N
+            tot["stats"] += E * s_in + mm + 8 * L.N * (-(-L.ng // 32))
+            tot["quantize"] += E * s_in + mm + packed + meta + 9 * L.N
         else:
             tot["quantize"] += E * s_in + packed + meta + 9 * L.N
         tot["dequantize"] += packed + meta + 9 * L.N + E * s_out
@@ -212,6 +216,9 @@ def config_dict(wl, args, world, n_loc):
         else "dp1",
         "l2": "inputs larger than L2: %.1f GB per step per GPU vs 126 MB L2" % (E * s_in / 1e9),
         "cuda_graph": bool(getattr(args, "graph", False)),
+        "metadata": ("bf16 (Z', R') word per group, 0.125 bits/elem (P:513)"
+                     if getattr(args, "meta", "f32") == "bf16"
+                     else "fp32 (zmin, scale) per group, 0.25 bits/elem"),
     }
 
 
@@ -314,7 +321,8 @@ def main():
                 dist.all_gather(list(S.view(world, -1).unbind(0)), S_loc)
     plan = ActivationSetPlan(xs, [W.quant_seed(t) for t in range(len(wl.acts))],
                              avg_bits=wl.avg_bits, bits=None if wl.avg_bits else wl.bits,
-                             n_total=n_total, sample_base=rank * n_loc, gather=gather)
+                             n_total=n_total, sample_base=rank * n_loc, gather=gather,
+                             meta=args.meta)
     max_numel = max(x.numel() for x in xs)
     outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(2)]
     out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
@@ -450,7 +458,8 @@ def main():
         with open(os.environ["ACTNN_LAYER_DUMP"], "w") as f:
             json.dump(rows, f, indent=0)
     bits_host = plan.bits_host()
-    alg = algorithmic_bytes(plan.layers, bits_host, s_in, s_in, plan.mixed)
+    alg = algorithmic_bytes(plan.layers, bits_host, s_in, s_in, plan.mixed,
+                            4 if args.meta == "bf16" else 8)
     peak, peak_src = hbm_peak()
     dom = max(kt, key=lambda k: kt[k])
     launches_dom = nl
@@ -460,7 +469,8 @@ def main():
                                            else "quantize_fast_kernel (K3)",
                                            "dequantize": "dequantize_fast_kernel (K4)"}[dom],
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "peak_source": peak_src, "traffic": ncu_traffic(dom, plan.mixed) if wl.name == "c3" else None,
+                "peak_source": peak_src, "traffic": (ncu_traffic(dom, plan.mixed)
+                            if wl.name == "c3" and args.meta == "f32" else None),
                 "algorithmic_bytes_per_launch": alg[dom] / launches_dom,
                 "avg_launch_us": kt[dom] * 1e3 / launches_dom,
                 "per_kernel": {k: {"ms_per_step": kt[k], "share_of_step": kt[k] / ms_step,

@@ -135,6 +135,32 @@ actnn_status_t actnn_dequantize(const uint8_t* packed, const float* zmin, const 
                                 const uint8_t* bits, const int64_t* off, int64_t N, int64_t D,
                                 int32_t G, void* out, actnn_dtype_t out_dt, void* stream);
 
+/* NEXT-1, bf16 metadata: the paper's storage format, "store the per-group range
+ * and zero points in bfloat16, so each group costs extra 32 bits, which is
+ * 0.125 bits on average" (the values are rounded
+ * BEFORE scaling, so the quantiser and the dequantiser use the same stored
+ * values).  meta [N*ng] u32, one word per group (4-byte aligned; 16-byte
+ * alignment with ng % 4 == 0 lets the dequantiser fetch it by TMA):
+ *   bits 0-15  Z' = bf16 of Z rounded toward -inf,
+ *   bits 16-31 R' = bf16 of RU(M - Z') rounded toward +inf,
+ * so [Z', Z' + R'] contains every element of the group (outward rounding,
+ * DESIGN reading 21).  Codes are those of actnn_quantize run with
+ * (Z, R) := (float(Z'), float(R')); all other arguments, layouts, ownership
+ * and errors as for actnn_quantize (zmin/scale are replaced by meta). */
+actnn_status_t actnn_quantize_bf16meta(const void* x, actnn_dtype_t dt, int64_t N, int64_t D,
+                                       int32_t G, const uint8_t* bits, const int64_t* off,
+                                       uint64_t seed, int64_t sample_base, const float* gmin,
+                                       const float* gmax, uint8_t* packed, uint32_t* meta,
+                                       void* stream);
+
+/* Decompressor for bf16 metadata: h_hat = fmaf(code, RN(float(R') / B),
+ * float(Z')), bf16 output RNE(h_hat).  Arguments as for actnn_dequantize with
+ * meta (as written by actnn_quantize_bf16meta) in place of zmin/scale. */
+actnn_status_t actnn_dequantize_bf16meta(const uint8_t* packed, const uint32_t* meta,
+                                         const uint8_t* bits, const int64_t* off, int64_t N,
+                                         int64_t D, int32_t G, void* out, actnn_dtype_t out_dt,
+                                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

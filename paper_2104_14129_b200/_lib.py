@@ -35,6 +35,10 @@ SIGNATURES = {
     "actnn_quantize": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I32, P, P, U64, I64, P, P, P,
                                       P, P, P]),
     "actnn_dequantize": (ctypes.c_int, [P, P, P, P, P, I64, I64, I32, P, ctypes.c_int, P]),
+    "actnn_quantize_bf16meta": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I32, P, P, U64, I64,
+                                               P, P, P, P, P]),
+    "actnn_dequantize_bf16meta": (ctypes.c_int, [P, P, P, P, I64, I64, I32, P, ctypes.c_int,
+                                                 P]),
 }
 
 
@@ -47,7 +51,7 @@ class ActnnError(RuntimeError):
 def header_symbols():
     """Function names declared in include/actnn.h."""
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(actnn_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(actnn_[a-z0-9_]+)\s*\(", txt)))
 
 
 def load():

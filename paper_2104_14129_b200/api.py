@@ -84,16 +84,21 @@ def packed_bytes(N: int, D: int, bits_host=None) -> int:
 
 @dataclass
 class Packed:
-    """A compressed activation (the saved context of P:578-592)."""
+    """A compressed activation (the saved context of P:578-592).
+
+    Metadata is either fp32 (zmin, scale) or, with meta="bf16" (NEXT-1, the
+    paper's P:513 format), one int32 word per group in ``meta``: bits 0-15 the
+    bf16 zero point Z', bits 16-31 the bf16 range R' (zmin/scale are None)."""
     packed: torch.Tensor      # uint8 code stream, sample n at off[n] - off[0]
-    zmin: torch.Tensor        # fp32 [N * ng]  zero points Z_ni
-    scale: torch.Tensor       # fp32 [N * ng]  R_ni / B_n
+    zmin: Optional[torch.Tensor]   # fp32 [N * ng]  zero points Z_ni
+    scale: Optional[torch.Tensor]  # fp32 [N * ng]  R_ni / B_n
     bits: torch.Tensor        # uint8 [N]      b_n
     off: torch.Tensor         # int64 [N + 1]  byte offsets
     shape: Tuple[int, ...]    # original activation shape
     dtype: torch.dtype        # original activation dtype
     seed: int
     sample_base: int
+    meta: Optional[torch.Tensor] = None  # int32 [N * ng] bf16 (Z', R') words
 
     @property
     def N(self) -> int:
@@ -107,8 +112,9 @@ class Packed:
         return n
 
     def nbytes(self) -> int:
-        return (self.packed.numel() + 4 * self.zmin.numel() + 4 * self.scale.numel()
-                + self.bits.numel() + 8 * self.off.numel())
+        meta = (4 * self.meta.numel() if self.meta is not None
+                else 4 * self.zmin.numel() + 4 * self.scale.numel())
+        return self.packed.numel() + meta + self.bits.numel() + 8 * self.off.numel()
 
 
 def group_stats(x: torch.Tensor, sens_out: Optional[torch.Tensor] = None):
@@ -158,11 +164,14 @@ def quantize(x: torch.Tensor, bits: torch.Tensor, off: torch.Tensor, seed: int,
              sample_base: int = 0, gmin: Optional[torch.Tensor] = None,
              gmax: Optional[torch.Tensor] = None, packed: Optional[torch.Tensor] = None,
              zmin: Optional[torch.Tensor] = None, scale: Optional[torch.Tensor] = None,
-             packed_nbytes: Optional[int] = None) -> Packed:
+             packed_nbytes: Optional[int] = None, meta: str = "f32",
+             meta_out: Optional[torch.Tensor] = None) -> Packed:
     """Compressor: per-group SR quantisation + packing.
 
     ``packed`` defaults to the 8-bit upper bound (bits live on the device);
-    pass ``packed_nbytes`` (e.g. read back from off[N]) to size it exactly."""
+    pass ``packed_nbytes`` (e.g. read back from off[N]) to size it exactly.
+    ``meta="bf16"``: the paper's bf16 metadata (NEXT-1) in one int32
+    word per group (``meta_out``) instead of fp32 zmin/scale."""
     x2 = _as_2d(x)
     N, D = x2.shape
     ng = ceil_div(D, G)
@@ -170,6 +179,17 @@ def quantize(x: torch.Tensor, bits: torch.Tensor, off: torch.Tensor, seed: int,
     if packed is None:
         nbytes = packed_nbytes if packed_nbytes is not None else N * ng * G
         packed = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    if meta == "bf16":
+        if meta_out is None:
+            meta_out = torch.empty(N * ng, dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().actnn_quantize_bf16meta(
+            _ptr(x2), _dtype_code(x2.dtype), N, D, G, _ptr(bits), _ptr(off),
+            ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), sample_base, _ptr(gmin), _ptr(gmax),
+            _ptr(packed), _ptr(meta_out), _stream(dev)))
+        return Packed(packed, None, None, bits, off, tuple(x.shape), x.dtype, seed, sample_base,
+                      meta_out)
+    if meta != "f32":
+        raise ActnnError(-1, f"unknown metadata format {meta!r} (f32 or bf16)")
     if zmin is None:
         zmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
     if scale is None:
@@ -187,6 +207,11 @@ def dequantize(p: Packed, out: Optional[torch.Tensor] = None,
     dev = p.packed.device
     if out is None:
         out = torch.empty(p.shape, dtype=out_dtype or p.dtype, device=dev)
+    if p.meta is not None:
+        _lib.check(_lib.load().actnn_dequantize_bf16meta(
+            _ptr(p.packed), _ptr(p.meta), _ptr(p.bits), _ptr(p.off), p.N, p.D, G, _ptr(out),
+            _dtype_code(out.dtype), _stream(dev)))
+        return out
     _lib.check(_lib.load().actnn_dequantize(
         _ptr(p.packed), _ptr(p.zmin), _ptr(p.scale), _ptr(p.bits), _ptr(p.off), p.N, p.D, G,
         _ptr(out), _dtype_code(out.dtype), _stream(dev)))
@@ -197,18 +222,19 @@ def compress(x: torch.Tensor, seed: int, bits: Optional[int] = None,
              avg_bits: Optional[float] = None, level_mask: int = LEVELS_POW2,
              sample_base: int = 0, gscale: Optional[torch.Tensor] = None,
              sens_allreduce: Optional[Callable[[torch.Tensor], torch.Tensor]] = None,
-             n_total: Optional[int] = None) -> Packed:
+             n_total: Optional[int] = None, meta: str = "f32") -> Packed:
     """One layer's compress call.
 
     bits=b: uniform b-bit (optimization level L2, single pass).
     avg_bits=a: per-sample mixed precision (L2.5): group_stats ->
     [sens_allreduce hook: sums the zero-padded S across ranks] -> greedy
-    allocation with budget floor(a * N_total) -> quantize with the stats."""
+    allocation with budget floor(a * N_total) -> quantize with the stats.
+    meta="bf16": the paper's bf16 per-group metadata (NEXT-1)."""
     x2 = _as_2d(x)
     N, D = x2.shape
     if bits is not None:
         b, o = uniform_bits(N, D, bits, x2.device)
-        return quantize(x, b, o, seed, sample_base)
+        return quantize(x, b, o, seed, sample_base, meta=meta)
     if avg_bits is None:
         raise ActnnError(-1, "compress needs bits= or avg_bits=")
     nt = n_total if n_total is not None else N
@@ -219,7 +245,8 @@ def compress(x: torch.Tensor, seed: int, bits: Optional[int] = None,
     budget = int(avg_bits * nt)
     bits_g, off_g = allocate_bits(S, budget, D, level_mask, gscale)
     lo = sample_base if nt != N else 0
-    return quantize(x, bits_g[lo:lo + N], off_g[lo:lo + N + 1], seed, sample_base, gmin, gmax)
+    return quantize(x, bits_g[lo:lo + N], off_g[lo:lo + N + 1], seed, sample_base, gmin, gmax,
+                    meta=meta)
 
 
 def decompress(p: Packed, out: Optional[torch.Tensor] = None) -> torch.Tensor:

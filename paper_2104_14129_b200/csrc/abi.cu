@@ -232,25 +232,29 @@ actnn_status_t actnn_uniform_bits(int64_t N, int64_t D, int32_t G, int32_t b, ui
                        "actnn_uniform_bits", s);
 }
 
-actnn_status_t actnn_quantize(const void* x, actnn_dtype_t dt, int64_t N, int64_t D, int32_t G,
-                              const uint8_t* bits, const int64_t* off, uint64_t seed,
-                              int64_t sample_base, const float* gmin, const float* gmax,
-                              uint8_t* packed, float* zmin, float* scale, void* stream) {
+// Shared body of actnn_quantize / actnn_quantize_bf16meta: exactly one of
+// (zmin, scale) and meta is in use.
+static actnn_status_t quantize_impl(const char* fn, const void* x, actnn_dtype_t dt, int64_t N,
+                                    int64_t D, int32_t G, const uint8_t* bits, const int64_t* off,
+                                    uint64_t seed, int64_t sample_base, const float* gmin,
+                                    const float* gmax, uint8_t* packed, float* zmin, float* scale,
+                                    uint32_t* meta, void* stream) {
     actnn_status_t st = common_checks(N, D, G);
     if (st) return st;
     if (!dtype_ok(dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)dt);
     if (sample_base < 0) return fail(ACTNN_ERR_INVALID, "negative sample_base");
     if (N == 0 || D == 0) return ACTNN_OK;
-    if (!x || !bits || !off || !packed || !zmin || !scale)
-        return fail(ACTNN_ERR_INVALID, "actnn_quantize: null pointer");
+    if (!x || !bits || !off || !packed || (meta ? false : (!zmin || !scale)))
+        return fail(ACTNN_ERR_INVALID, "%s: null pointer", fn);
     if ((gmin == nullptr) != (gmax == nullptr))
-        return fail(ACTNN_ERR_INVALID, "actnn_quantize: gmin and gmax must both be set or NULL");
+        return fail(ACTNN_ERR_INVALID, "%s: gmin and gmax must both be set or NULL", fn);
     const size_t es = dt == ACTNN_F32 ? 4 : 2;
-    if (!aligned(x, es) || !aligned(off, 8) || !aligned(zmin, 4) || !aligned(scale, 4) ||
+    if (!aligned(x, es) || !aligned(off, 8) || (zmin && !aligned(zmin, 4)) ||
+        (scale && !aligned(scale, 4)) || (meta && !aligned(meta, 4)) ||
         (gmin && (!aligned(gmin, 4) || !aligned(gmax, 4))))
-        return fail(ACTNN_ERR_INVALID, "actnn_quantize: misaligned pointer");
+        return fail(ACTNN_ERR_INVALID, "%s: misaligned pointer", fn);
     if (!aligned(packed, 16))
-        return fail(ACTNN_ERR_UNSUPPORTED, "actnn_quantize: packed must be 16-byte aligned");
+        return fail(ACTNN_ERR_UNSUPPORTED, "%s: packed must be 16-byte aligned", fn);
     const int64_t ng = ceil_div(D, G);
     st = debug_validate(bits, off, N, ng, (cudaStream_t)stream);
     if (st) return st;
@@ -267,34 +271,58 @@ actnn_status_t actnn_quantize(const void* x, actnn_dtype_t dt, int64_t N, int64_
     a.gmin = gmin;
     a.gmax = gmax;
     a.packed = packed;
-    a.zmin = zmin;
-    a.scale = scale;
+    a.zmin = meta ? nullptr : zmin;
+    a.scale = meta ? nullptr : scale;
+    a.meta = meta;
     a.fast = (D % G == 0) && aligned(x, dt == ACTNN_F32 ? 32 : 16);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    return post_launch(launch_quantize(a, s), "actnn_quantize", s);
+    return post_launch(launch_quantize(a, s), fn, s);
 }
 
-actnn_status_t actnn_dequantize(const uint8_t* packed, const float* zmin, const float* scale,
-                                const uint8_t* bits, const int64_t* off, int64_t N, int64_t D,
-                                int32_t G, void* out, actnn_dtype_t out_dt, void* stream) {
+actnn_status_t actnn_quantize(const void* x, actnn_dtype_t dt, int64_t N, int64_t D, int32_t G,
+                              const uint8_t* bits, const int64_t* off, uint64_t seed,
+                              int64_t sample_base, const float* gmin, const float* gmax,
+                              uint8_t* packed, float* zmin, float* scale, void* stream) {
+    return quantize_impl("actnn_quantize", x, dt, N, D, G, bits, off, seed, sample_base, gmin,
+                         gmax, packed, zmin, scale, nullptr, stream);
+}
+
+actnn_status_t actnn_quantize_bf16meta(const void* x, actnn_dtype_t dt, int64_t N, int64_t D,
+                                       int32_t G, const uint8_t* bits, const int64_t* off,
+                                       uint64_t seed, int64_t sample_base, const float* gmin,
+                                       const float* gmax, uint8_t* packed, uint32_t* meta,
+                                       void* stream) {
+    if (N > 0 && D > 0 && !meta)
+        return fail(ACTNN_ERR_INVALID, "actnn_quantize_bf16meta: null pointer");
+    return quantize_impl("actnn_quantize_bf16meta", x, dt, N, D, G, bits, off, seed, sample_base,
+                         gmin, gmax, packed, nullptr, nullptr, meta, stream);
+}
+
+static actnn_status_t dequantize_impl(const char* fn, const uint8_t* packed, const float* zmin,
+                                      const float* scale, const uint32_t* meta,
+                                      const uint8_t* bits, const int64_t* off, int64_t N,
+                                      int64_t D, int32_t G, void* out, actnn_dtype_t out_dt,
+                                      void* stream) {
     actnn_status_t st = common_checks(N, D, G);
     if (st) return st;
     if (!dtype_ok(out_dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)out_dt);
     if (N == 0 || D == 0) return ACTNN_OK;
-    if (!packed || !zmin || !scale || !bits || !off || !out)
-        return fail(ACTNN_ERR_INVALID, "actnn_dequantize: null pointer");
+    if (!packed || (meta ? false : (!zmin || !scale)) || !bits || !off || !out)
+        return fail(ACTNN_ERR_INVALID, "%s: null pointer", fn);
     const size_t es = out_dt == ACTNN_F32 ? 4 : 2;
-    if (!aligned(out, es) || !aligned(off, 8) || !aligned(zmin, 4) || !aligned(scale, 4))
-        return fail(ACTNN_ERR_INVALID, "actnn_dequantize: misaligned pointer");
+    if (!aligned(out, es) || !aligned(off, 8) || (zmin && !aligned(zmin, 4)) ||
+        (scale && !aligned(scale, 4)) || (meta && !aligned(meta, 4)))
+        return fail(ACTNN_ERR_INVALID, "%s: misaligned pointer", fn);
     if (!aligned(packed, 16))
-        return fail(ACTNN_ERR_UNSUPPORTED, "actnn_dequantize: packed must be 16-byte aligned");
+        return fail(ACTNN_ERR_UNSUPPORTED, "%s: packed must be 16-byte aligned", fn);
     const int64_t ng = ceil_div(D, G);
     st = debug_validate(bits, off, N, ng, (cudaStream_t)stream);
     if (st) return st;
     DequantArgs a;
     a.packed = packed;
-    a.zmin = zmin;
-    a.scale = scale;
+    a.zmin = meta ? nullptr : zmin;
+    a.scale = meta ? nullptr : scale;
+    a.meta = meta;
     a.bits = bits;
     a.off = off;
     a.N = N;
@@ -304,7 +332,24 @@ actnn_status_t actnn_dequantize(const uint8_t* packed, const float* zmin, const 
     a.out_dt = (int)out_dt;
     a.fast = (D % G == 0) && aligned(out, out_dt == ACTNN_F32 ? 32 : 16);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    return post_launch(launch_dequantize(a, s), "actnn_dequantize", s);
+    return post_launch(launch_dequantize(a, s), fn, s);
+}
+
+actnn_status_t actnn_dequantize(const uint8_t* packed, const float* zmin, const float* scale,
+                                const uint8_t* bits, const int64_t* off, int64_t N, int64_t D,
+                                int32_t G, void* out, actnn_dtype_t out_dt, void* stream) {
+    return dequantize_impl("actnn_dequantize", packed, zmin, scale, nullptr, bits, off, N, D, G,
+                           out, out_dt, stream);
+}
+
+actnn_status_t actnn_dequantize_bf16meta(const uint8_t* packed, const uint32_t* meta,
+                                         const uint8_t* bits, const int64_t* off, int64_t N,
+                                         int64_t D, int32_t G, void* out, actnn_dtype_t out_dt,
+                                         void* stream) {
+    if (N > 0 && D > 0 && !meta)
+        return fail(ACTNN_ERR_INVALID, "actnn_dequantize_bf16meta: null pointer");
+    return dequantize_impl("actnn_dequantize_bf16meta", packed, nullptr, nullptr, meta, bits, off,
+                           N, D, G, out, out_dt, stream);
 }
 
 }  // extern "C"

@@ -31,6 +31,7 @@ struct DParams {
     const uint8_t* packed;
     const float* zmin;
     const float* scale;
+    const uint32_t* meta;  // NEXT-1 bf16 words (kB16)
     const uint8_t* bits;
     const int64_t* off;
     uint32_t N, D, ng, nb;
@@ -42,6 +43,7 @@ struct GDParams {  // generic kernel
     const uint8_t* packed;
     const float* zmin;
     const float* scale;
+    const uint32_t* meta;  // NEXT-1 bf16 words, or null
     const uint8_t* bits;
     const int64_t* off;
     int64_t N, D, ng;
@@ -96,11 +98,10 @@ __device__ __forceinline__ void dequant_group(uint64_t pay, float Z, float s, TO
     store8(dst, o);
 }
 
-// A unit: zq/sq point at the 4 zero points / scales (shared memory when they
-// came with the stage, global otherwise).
+// A unit: zq/sq = the unit's 4 zero points / scales.
 template <typename TO, int b, bool kFullUnit>
-__device__ __forceinline__ void dequant_unit(const uint8_t* st, int gcount, const float* zq,
-                                             const float* sq, TO* dst, int lane) {
+__device__ __forceinline__ void dequant_unit(const uint8_t* st, int gcount, const float (&zq)[kU],
+                                             const float (&sq)[kU], TO* dst, int lane) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
         if (kFullUnit || u < gcount) {
@@ -111,8 +112,9 @@ __device__ __forceinline__ void dequant_unit(const uint8_t* st, int gcount, cons
 }
 
 template <typename TO, int b>
-__device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount, const float* zq,
-                                                 const float* sq, TO* dst, int lane) {
+__device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount,
+                                                 const float (&zq)[kU], const float (&sq)[kU],
+                                                 TO* dst, int lane) {
     if (gcount == kU)
         dequant_unit<TO, b, true>(st, gcount, zq, sq, dst, lane);
     else
@@ -120,8 +122,10 @@ __device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount, 
 }
 
 // kCached: (bits, off) of all samples in shared memory (N <= kNCap).
-// kMeta: the unit's (zmin, scale) travel in the stage (ng % 4 == 0).
-template <typename TO, bool kCached, bool kMeta>
+// kMeta: the unit's metadata travels in the stage (ng % 4 == 0).
+// kB16: NEXT-1 bf16 metadata words (Z', R'): lane u < 4 widens group u's word
+// and computes scale = RN(R' / B) once, the unit's lanes get it by shuffle.
+template <typename TO, bool kCached, bool kMeta, bool kB16>
 __global__ void __launch_bounds__(kBlock, 3)
     dequantize_fast_kernel(const __grid_constant__ DParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -165,7 +169,11 @@ __global__ void __launch_bounds__(kBlock, 3)
         const int64_t sofs = kCached ? ((int64_t)s_off[pn] << 5) : (p.off[pn] - off0);
         const uint32_t bytes = (uint32_t)(gcount_of(pj) * 32 * b);
         uint8_t* dst = ring + s * kStage;
-        if (kMeta) {
+        if (kMeta && kB16) {
+            const uint32_t g = pn * p.ng + pj * kU;
+            mbar_expect_tx(&bars[s], bytes + 16);
+            bulk_g2s(dst + kPay, p.meta + g, 16, &bars[s]);
+        } else if (kMeta) {
             const uint32_t g = pn * p.ng + pj * kU;
             mbar_expect_tx(&bars[s], bytes + 32);
             bulk_g2s(dst + kPay, p.zmin + g, 16, &bars[s]);
@@ -193,9 +201,27 @@ __global__ void __launch_bounds__(kBlock, 3)
         TO* dst = out + (uint64_t)n * p.D + (uint64_t)j * (kU * kG);
         const uint8_t* st = ring + stage * kStage;
         const uint32_t g = n * p.ng + j * kU;
-        const float* zq = kMeta ? reinterpret_cast<const float*>(st + kPay) : p.zmin + g;
-        const float* sq = kMeta ? reinterpret_cast<const float*>(st + kPay + 16) : p.scale + g;
         mbar_wait(&bars[stage], phase);
+        float zq[kU], sq[kU];
+        if constexpr (kB16) {
+            const uint32_t* wq = kMeta ? reinterpret_cast<const uint32_t*>(st + kPay) : p.meta + g;
+            const uint32_t wl = lane < gcount ? wq[lane] : 0u;
+            const float zl = meta_zero(wl);
+            const float sl = meta_scale(wl, (b >= 1 && b <= 8) ? b : 1);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                zq[u] = __shfl_sync(0xffffffffu, zl, u);
+                sq[u] = __shfl_sync(0xffffffffu, sl, u);
+            }
+        } else {
+            const float* zp = kMeta ? reinterpret_cast<const float*>(st + kPay) : p.zmin + g;
+            const float* sp = kMeta ? reinterpret_cast<const float*>(st + kPay + 16) : p.scale + g;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                zq[u] = u < gcount ? zp[u] : 0.0f;
+                sq[u] = u < gcount ? sp[u] : 0.0f;
+            }
+        }
         if (b == 2) dequant_unit_any<TO, 2>(st, gcount, zq, sq, dst, lane);
         else if (b == 1) dequant_unit_any<TO, 1>(st, gcount, zq, sq, dst, lane);
         else if (b == 4) dequant_unit_any<TO, 4>(st, gcount, zq, sq, dst, lane);
@@ -236,8 +262,15 @@ __global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(const __grid
         const uint8_t* seg = p.packed + (p.off[n] - off0) + i * 32 * b;
         uint64_t pay = 0;
         for (int t = 0; t < b; ++t) pay |= (uint64_t)__ldg(seg + lane * b + t) << (8 * t);
-        const float Z = __ldg(p.zmin + g);
-        const float s = __ldg(p.scale + g);
+        float Z, s;
+        if (p.meta) {
+            const uint32_t w = __ldg(p.meta + g);
+            Z = meta_zero(w);
+            s = meta_scale(w, b);
+        } else {
+            Z = __ldg(p.zmin + g);
+            s = __ldg(p.scale + g);
+        }
         const uint32_t mask = (1u << b) - 1u;
         TO* dst = out + n * p.D + i * kG;
 #pragma unroll
@@ -248,9 +281,9 @@ __global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(const __grid
     }
 }
 
-template <typename TO, bool kCached, bool kMeta>
+template <typename TO, bool kCached, bool kMeta, bool kB16>
 void launch_fast(const DParams& p0, int64_t units, cudaStream_t s) {
-    const void* k = (const void*)dequantize_fast_kernel<TO, kCached, kMeta>;
+    const void* k = (const void*)dequantize_fast_kernel<TO, kCached, kMeta, kB16>;
     static bool attr = false;  // one-time opt-in above 48 KB of dynamic smem
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
@@ -261,7 +294,7 @@ void launch_fast(const DParams& p0, int64_t units, cudaStream_t s) {
     const uint32_t nwarps = (uint32_t)grid * kWarps;
     p.step_n = nwarps / p.nb;
     p.step_j = nwarps % p.nb;
-    dequantize_fast_kernel<TO, kCached, kMeta><<<grid, kBlock, kSmem, s>>>(p);
+    dequantize_fast_kernel<TO, kCached, kMeta, kB16><<<grid, kBlock, kSmem, s>>>(p);
 }
 
 template <typename TO>
@@ -273,6 +306,7 @@ cudaError_t run(const DequantArgs& a, cudaStream_t s) {
         p.packed = a.packed;
         p.zmin = a.zmin;
         p.scale = a.scale;
+        p.meta = a.meta;
         p.bits = a.bits;
         p.off = a.off;
         p.N = (uint32_t)a.N;
@@ -282,16 +316,25 @@ cudaError_t run(const DequantArgs& a, cudaStream_t s) {
         p.step_n = p.step_j = 0;
         p.out = a.out;
         const bool cached = a.N <= kNCap;
-        // metadata by TMA: every unit's 4 floats start 16-byte aligned
-        const bool meta = (a.ng % kU == 0) && ((uintptr_t)a.zmin % 16 == 0) &&
-                          ((uintptr_t)a.scale % 16 == 0);
+        // metadata by TMA: every unit's 4 floats / words start 16-byte aligned
+        const bool b16 = a.meta != nullptr;
+        const bool meta = (a.ng % kU == 0) &&
+                          (b16 ? (uintptr_t)a.meta % 16 == 0
+                               : ((uintptr_t)a.zmin % 16 == 0) && ((uintptr_t)a.scale % 16 == 0));
         const int64_t units = a.N * nb;
-        if (cached && meta) launch_fast<TO, true, true>(p, units, s);
-        else if (cached) launch_fast<TO, true, false>(p, units, s);
-        else if (meta) launch_fast<TO, false, true>(p, units, s);
-        else launch_fast<TO, false, false>(p, units, s);
+        if (b16) {
+            if (cached && meta) launch_fast<TO, true, true, true>(p, units, s);
+            else if (cached) launch_fast<TO, true, false, true>(p, units, s);
+            else if (meta) launch_fast<TO, false, true, true>(p, units, s);
+            else launch_fast<TO, false, false, true>(p, units, s);
+        } else {
+            if (cached && meta) launch_fast<TO, true, true, false>(p, units, s);
+            else if (cached) launch_fast<TO, true, false, false>(p, units, s);
+            else if (meta) launch_fast<TO, false, true, false>(p, units, s);
+            else launch_fast<TO, false, false, false>(p, units, s);
+        }
     } else {
-        GDParams p{a.packed, a.zmin, a.scale, a.bits, a.off, a.N, a.D, a.ng, a.out};
+        GDParams p{a.packed, a.zmin, a.scale, a.meta, a.bits, a.off, a.N, a.D, a.ng, a.out};
         const int grid = grid_for((const void*)dequantize_generic_kernel<TO>, kBlock, 0,
                                   (a.N * a.ng + kWarps - 1) / kWarps);
         dequantize_generic_kernel<TO><<<grid, kBlock, 0, s>>>(p);

@@ -191,6 +191,40 @@ __device__ __forceinline__ GroupConst group_const(float mn, float mx, int b) {
     return c;
 }
 
+// NEXT-1, bf16 metadata ("stored and used values identical";
+// DESIGN reading 21): Z' = bf16 toward -inf of Z, R' = bf16 toward +inf of
+// RU(M - Z'); the word holds Z' (bits 0-15) and R' (bits 16-31), and the
+// quantiser runs O4-O8 on (float(Z'), float(R')).  bf16 = the high half of an
+// fp32, whose bit pattern is monotone in magnitude for a fixed sign.
+struct GroupConstB {
+    float Z, inv14;
+    uint32_t word;
+};
+
+__device__ __forceinline__ GroupConstB group_const_bf16(float mn, float mx, int b) {
+    const float Z = __fadd_rn(mn, 0.0f);
+    const float M = __fadd_rn(mx, 0.0f);
+    const uint32_t zu = __float_as_uint(Z);
+    const uint32_t zb = (zu >> 16) + (((zu & 0xFFFFu) != 0u) & (zu >> 31));  // toward -inf
+    const float Zp = __uint_as_float(zb << 16);
+    const uint32_t tu = __float_as_uint(__fsub_ru(M, Zp));                    // >= +0
+    const uint32_t rb = (tu >> 16) + ((tu & 0xFFFFu) != 0u);                  // toward +inf
+    const float Rp = __uint_as_float(rb << 16);
+    const float Bf = (float)((1u << b) - 1u);
+    GroupConstB c;
+    c.Z = Zp;
+    c.inv14 = (Rp < 0x1p-96f) ? 0.0f : __fmul_rn(__fdiv_rn(Bf, Rp), 16384.0f);
+    c.word = (zb & 0xFFFFu) | (rb << 16);
+    return c;
+}
+
+// The dequantiser's (Z, scale) from a bf16 metadata word: float(Z'),
+// RN(float(R') / B) (O10 with the stored values).
+__device__ __forceinline__ float meta_zero(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float meta_scale(uint32_t w, int b) {
+    return __fdiv_rn(__uint_as_float(w & 0xFFFF0000u), (float)((1u << b) - 1u));
+}
+
 // ACTNN-Q v1 O5 + O7: q = RNE((h - Z) * inv14) as an integer in [0, B*2^14],
 // obtained exactly from one fma against 1.5*2^23 (the sum stays in
 // [2^23, 2^24) where the ulp is 1; the constant is even so ties agree with

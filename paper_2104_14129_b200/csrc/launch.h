@@ -19,6 +19,7 @@ struct QuantArgs {
     uint8_t* packed;
     float* zmin;
     float* scale;
+    uint32_t* meta;  // NEXT-1 bf16 metadata words (then zmin/scale are null), or null
     bool fast;  // D % 256 == 0 and x aligned for vector loads
 };
 
@@ -26,6 +27,7 @@ struct DequantArgs {
     const uint8_t* packed;
     const float* zmin;
     const float* scale;
+    const uint32_t* meta;  // NEXT-1 bf16 metadata words (then zmin/scale are null), or null
     const uint8_t* bits;
     const int64_t* off;
     int64_t N, D, ng;

@@ -89,6 +89,7 @@ struct QParams {
     uint8_t* packed;
     float* zmin;
     float* scale;
+    uint32_t* meta;  // bf16 metadata words (NEXT-1) instead of zmin/scale, or null
     RoundKeys rk;
 };
 
@@ -103,8 +104,29 @@ struct GParams {  // generic kernel
     uint8_t* packed;
     float* zmin;
     float* scale;
+    uint32_t* meta;
     RoundKeys rk;
 };
+
+// Group constants of either metadata format; stores this group's metadata.
+__device__ __forceinline__ void group_const_store(float mn, float mx, int b, uint32_t* meta,
+                                                  float* zm, float* sc, bool store, float& Z,
+                                                  float& inv14) {
+    if (meta) {  // NEXT-1: bf16 words, quantise with the stored values
+        const GroupConstB c = group_const_bf16(mn, mx, b);
+        if (store) *meta = c.word;
+        Z = c.Z;
+        inv14 = c.inv14;
+    } else {
+        const GroupConst c = group_const(mn, mx, b);
+        if (store) {
+            *zm = c.Z;
+            *sc = c.scale;
+        }
+        Z = c.Z;
+        inv14 = c.inv14;
+    }
+}
 
 // Codes of a lane's 8 elements for b in {1, 2}, packed LSB-first (O8) into the
 // low 8 b bits.  Pair p = elements (2p, 2p+1) uses Philox word p, whose low
@@ -198,18 +220,17 @@ __device__ __forceinline__ void quant_group(const float v[8], float Z, float inv
 // u of the unit), then codes + packing of each group.  kFullUnit: gcount == U.
 template <int b, bool kFullUnit>
 __device__ __forceinline__ void quant_unit(const float (&v)[kU][8], int gcount, float myMn,
-                                           float myMx, float* zm, float* sc, uint8_t* seg,
-                                           uint64_t blk0, const RoundKeys& rk, int lane) {
-    const GroupConst cc = group_const(myMn, myMx, b);
-    if (lane < (kFullUnit ? kU : gcount)) {
-        zm[lane] = cc.Z;
-        sc[lane] = cc.scale;
-    }
+                                           float myMx, float* zm, float* sc, uint32_t* mw,
+                                           uint8_t* seg, uint64_t blk0, const RoundKeys& rk,
+                                           int lane) {
+    float cZ, cInv;
+    group_const_store(myMn, myMx, b, mw ? mw + lane : nullptr, zm + lane, sc + lane,
+                      lane < (kFullUnit ? kU : gcount), cZ, cInv);
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
         if (kFullUnit || u < gcount) {
-            const float Z = __shfl_sync(kFull, cc.Z, u);
-            const float inv = __shfl_sync(kFull, cc.inv14, u);
+            const float Z = __shfl_sync(kFull, cZ, u);
+            const float inv = __shfl_sync(kFull, cInv, u);
             quant_group<b>(v[u], Z, inv, blk0 + (uint64_t)(u * 32 + lane), rk, seg + u * 32 * b,
                            lane);
         }
@@ -218,12 +239,13 @@ __device__ __forceinline__ void quant_unit(const float (&v)[kU][8], int gcount, 
 
 template <int b>
 __device__ __forceinline__ void quant_unit_any(const float (&v)[kU][8], int gcount, float myMn,
-                                               float myMx, float* zm, float* sc, uint8_t* seg,
-                                               uint64_t blk0, const RoundKeys& rk, int lane) {
+                                               float myMx, float* zm, float* sc, uint32_t* mw,
+                                               uint8_t* seg, uint64_t blk0, const RoundKeys& rk,
+                                               int lane) {
     if (gcount == kU)
-        quant_unit<b, true>(v, gcount, myMn, myMx, zm, sc, seg, blk0, rk, lane);
+        quant_unit<b, true>(v, gcount, myMn, myMx, zm, sc, mw, seg, blk0, rk, lane);
     else
-        quant_unit<b, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, rk, lane);
+        quant_unit<b, false>(v, gcount, myMn, myMx, zm, sc, mw, seg, blk0, rk, lane);
 }
 
 template <typename T, bool kStats, bool kCached>
@@ -348,15 +370,20 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
         const uint64_t blk0 = (uint64_t)(p.sample_base + n) * (p.D >> 3) + (uint64_t)gi * 32;
         float* zm = p.zmin + g;
         float* sc = p.scale + g;
+        uint32_t* mw = p.meta ? p.meta + g : nullptr;
+#define ACTNN_QU(B) quant_unit_any<B>(v, gcount, myMn, myMx, zm, sc, mw, seg, blk0, p.rk, lane)
+#define ACTNN_QG(B) quant_unit<B, false>(v, gcount, myMn, myMx, zm, sc, mw, seg, blk0, p.rk, lane)
         switch (b) {
-            case 1: quant_unit_any<1>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
-            case 2: quant_unit_any<2>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
-            case 4: quant_unit_any<4>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
-            case 8: quant_unit_any<8>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
-            case 3: quant_unit<3, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
-            case 5: quant_unit<5, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
-            case 6: quant_unit<6, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
-            case 7: quant_unit<7, false>(v, gcount, myMn, myMx, zm, sc, seg, blk0, p.rk, lane); break;
+            case 1: ACTNN_QU(1); break;
+            case 2: ACTNN_QU(2); break;
+            case 4: ACTNN_QU(4); break;
+            case 8: ACTNN_QU(8); break;
+            case 3: ACTNN_QG(3); break;
+            case 5: ACTNN_QG(5); break;
+            case 6: ACTNN_QG(6); break;
+            case 7: ACTNN_QG(7); break;
+#undef ACTNN_QU
+#undef ACTNN_QG
             default: break;  // invalid width: outside the contract (ACTNN_CHECK=1 reports it)
         }
         if (++stage == S) {
@@ -405,11 +432,9 @@ __global__ void __launch_bounds__(kBlock) quantize_generic_kernel(const __grid_c
             mn = __ldg(p.gmin + g);
             mx = __ldg(p.gmax + g);
         }
-        const GroupConst cc = group_const(mn, mx, b);
-        if (lane == 0) {
-            p.zmin[g] = cc.Z;
-            p.scale[g] = cc.scale;
-        }
+        float cZ, cInv;
+        group_const_store(mn, mx, b, p.meta ? p.meta + g : nullptr, p.zmin + g, p.scale + g,
+                          lane == 0, cZ, cInv);
         const uint64_t e_first =
             (uint64_t)(p.sample_base + n) * (uint64_t)p.D + (uint64_t)(i * kG + lane * 8);
         const uint64_t blkA = e_first >> 3;
@@ -423,7 +448,7 @@ __global__ void __launch_bounds__(kBlock) quantize_generic_kernel(const __grid_c
             const uint64_t e = e_first + jj;
             const uint32_t r =
                 ((e >> 3) == blkA) ? rnd14(oA, (int)(e & 7)) : rnd14(oB, (int)(e & 7));
-            const uint32_t code = idx < len ? sr_code(v[jj], cc.Z, cc.inv14, r) : 0u;
+            const uint32_t code = idx < len ? sr_code(v[jj], cZ, cInv, r) : 0u;
             pk |= (uint64_t)code << (b * jj);
         }
         uint8_t* seg = p.packed + (p.off[n] - off0) + i * 32 * b;
@@ -452,6 +477,7 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
         p.packed = a.packed;
         p.zmin = a.zmin;
         p.scale = a.scale;
+        p.meta = a.meta;
         p.rk = make_round_keys(a.seed);
         const bool cached = a.N <= kNCap;
         const void* k = cached ? (const void*)quantize_fast_kernel<T, kStats, true>
@@ -485,6 +511,7 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
         p.packed = a.packed;
         p.zmin = a.zmin;
         p.scale = a.scale;
+        p.meta = a.meta;
         p.rk = make_round_keys(a.seed);
         const void* k = (const void*)quantize_generic_kernel<T, kStats>;
         const int grid = grid_for(k, kBlock, 0, (a.N * a.ng + kWarps - 1) / kWarps);

@@ -88,6 +88,7 @@ struct WSParams {
     uint8_t* packed;
     float* zmin;
     float* scale;
+    uint32_t* meta;  // NEXT-1 bf16 metadata words instead of zmin/scale, or null
     RoundKeys rk;
 };
 
@@ -455,11 +456,18 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
                 for (int t = 0; t < GPL; ++t) {
                     const int k = kl + t * LPC;
                     if (k < gcount) {
-                        const GroupConst cc = group_const(cmn[t], cmx[t], b);
-                        p.zmin[g + k] = cc.Z;
-                        p.scale[g + k] = cc.scale;
-                        d.Z[k] = cc.Z;
-                        d.inv[k] = cc.inv14;
+                        if (p.meta) {  // NEXT-1: bf16 words; quantise with the stored values
+                            const GroupConstB cc = group_const_bf16(cmn[t], cmx[t], b);
+                            p.meta[g + k] = cc.word;
+                            d.Z[k] = cc.Z;
+                            d.inv[k] = cc.inv14;
+                        } else {
+                            const GroupConst cc = group_const(cmn[t], cmx[t], b);
+                            p.zmin[g + k] = cc.Z;
+                            p.scale[g + k] = cc.scale;
+                            d.Z[k] = cc.Z;
+                            d.inv[k] = cc.inv14;
+                        }
                     }
                 }
                 if (kl == 0) {
@@ -558,6 +566,7 @@ cudaError_t run_ws(const QuantArgs& a, cudaStream_t s) {
     p.packed = a.packed;
     p.zmin = a.zmin;
     p.scale = a.scale;
+    p.meta = a.meta;
     p.rk = make_round_keys(a.seed);
     const int64_t units = a.N * (int64_t)p.nb;
     if (a.N <= kNCap)

@@ -47,6 +47,7 @@ class Layer:
     packed: torch.Tensor = None
     zmin: torch.Tensor = None
     scale: torch.Tensor = None
+    meta: torch.Tensor = None       # int32 [N * ng] bf16 (Z', R') words (meta="bf16")
     args: dict = field(default_factory=dict)
 
 
@@ -55,10 +56,18 @@ class ActivationSetPlan:
                  avg_bits: Optional[float] = None, bits: Optional[int] = None,
                  level_mask: int = LEVELS_POW2, n_total: Optional[int] = None,
                  sample_base: int = 0,
-                 gather: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None):
+                 gather: Optional[Callable[[torch.Tensor, torch.Tensor], None]] = None,
+                 meta: str = "f32"):
         if (avg_bits is None) == (bits is None):
             raise ValueError("give exactly one of avg_bits / bits")
+        if meta not in ("f32", "bf16"):
+            raise ValueError(f"unknown metadata format {meta!r}")
         self.lib = _lib.load()
+        # metadata format: fp32 (zmin, scale) or the paper's bf16 words (NEXT-1)
+        self.meta = meta
+        self.qfn = self.lib.actnn_quantize if meta == "f32" else self.lib.actnn_quantize_bf16meta
+        self.dfn = (self.lib.actnn_dequantize if meta == "f32"
+                    else self.lib.actnn_dequantize_bf16meta)
         self.mixed = avg_bits is not None
         # k > 1: gather(S_global, S_local) fills S_global[N_total] with every
         # rank's S_n (an all-gather over NCCL: the exchange step, equivalent
@@ -81,8 +90,13 @@ class ActivationSetPlan:
             # min(8 N, budget) * unit bytes.
             cap = min(8 * N, budget) * unit
             L.packed = torch.empty(max(cap, 16), dtype=torch.uint8, device=dev)
-            L.zmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
-            L.scale = torch.empty(N * ng, dtype=torch.float32, device=dev)
+            if meta == "f32":
+                L.zmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
+                L.scale = torch.empty(N * ng, dtype=torch.float32, device=dev)
+                mq = (_p(L.zmin), _p(L.scale))
+            else:
+                L.meta = torch.empty(N * ng, dtype=torch.int32, device=dev)
+                mq = (_p(L.meta),)
             L.bits = torch.empty(nt, dtype=torch.uint8, device=dev)
             L.off = torch.empty(nt + 1, dtype=torch.int64, device=dev)
             lo = sample_base if nt != N else 0
@@ -100,16 +114,14 @@ class ActivationSetPlan:
                 L.args["alloc"] = (_p(L.S), None, nt, budget, level_mask, D, G, _p(L.bits),
                                    _p(L.off), None, 0)
                 L.args["quant"] = (_p(x2), dt, N, D, G, bits_p, off_p, ctypes.c_uint64(seed),
-                                   sample_base, _p(L.gmin), _p(L.gmax), _p(L.packed),
-                                   _p(L.zmin), _p(L.scale))
+                                   sample_base, _p(L.gmin), _p(L.gmax), _p(L.packed)) + mq
             else:
                 # L2: fixed widths, written once (not part of a step)
                 _lib.check(lib.actnn_uniform_bits(nt, D, G, bits, _p(L.bits), _p(L.off),
                                                   _P(torch.cuda.current_stream(dev).cuda_stream)))
                 L.args["quant"] = (_p(x2), dt, N, D, G, bits_p, off_p, ctypes.c_uint64(seed),
-                                   sample_base, None, None, _p(L.packed), _p(L.zmin),
-                                   _p(L.scale))
-            L.args["dequant"] = (_p(L.packed), _p(L.zmin), _p(L.scale), bits_p, off_p, N, D, G)
+                                   sample_base, None, None, _p(L.packed)) + mq
+            L.args["dequant"] = (_p(L.packed),) + mq + (bits_p, off_p, N, D, G)
             self.layers.append(L)
 
     # launches per step: stats (K1 with K1b fused) + allocate + quantize + dequantize
@@ -129,7 +141,7 @@ class ActivationSetPlan:
             _lib.check(lib.actnn_allocate_bits(*L.args["alloc"], stream))
         if ev is not None:
             ev[2].record()
-        _lib.check(lib.actnn_quantize(*L.args["quant"], stream))
+        _lib.check(self.qfn(*L.args["quant"], stream))
         if ev is not None:
             ev[3].record()
 
@@ -137,7 +149,7 @@ class ActivationSetPlan:
         L = self.layers[i]
         if ev is not None:
             ev[0].record()
-        _lib.check(self.lib.actnn_dequantize(*L.args["dequant"], _p(out), out_dt, stream))
+        _lib.check(self.dfn(*L.args["dequant"], _p(out), out_dt, stream))
         if ev is not None:
             ev[1].record()
 
@@ -158,7 +170,7 @@ class ActivationSetPlan:
         if not self.mixed:
             sp = _P(main.cuda_stream)
             for i in range(len(self.layers)):
-                _lib.check(self.lib.actnn_quantize(*self.layers[i].args["quant"], sp))
+                _lib.check(self.qfn(*self.layers[i].args["quant"], sp))
             return
         lib = self.lib
         if getattr(self, "_evs2", None) is None:
@@ -179,7 +191,7 @@ class ActivationSetPlan:
             ev_alloc.record(alloc)
         for i, L in enumerate(self.layers):
             main.wait_event(self._evs2[i][1])
-            _lib.check(lib.actnn_quantize(*L.args["quant"], sm))
+            _lib.check(self.qfn(*L.args["quant"], sm))
 
     def decompress_all(self, outs: Sequence[torch.Tensor], out_dt: int,
                        streams: Sequence[torch.cuda.Stream]):
@@ -191,8 +203,8 @@ class ActivationSetPlan:
             s.wait_stream(streams[0])
         sps = [_P(s.cuda_stream) for s in streams]
         for i, L in enumerate(self.layers):
-            _lib.check(self.lib.actnn_dequantize(*L.args["dequant"], _p(outs[i % len(outs)]),
-                                                 out_dt, sps[i % k]))
+            _lib.check(self.dfn(*L.args["dequant"], _p(outs[i % len(outs)]), out_dt,
+                                sps[i % k]))
         for s in streams[1:]:
             streams[0].wait_stream(s)
 

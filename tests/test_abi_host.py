@@ -19,7 +19,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = _lib.header_symbols()
-    assert len(names) == 9
+    assert len(names) == 11
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_lib.SIGNATURES)
@@ -83,6 +83,24 @@ def test_dequantize_and_stats_host_validation(lib):
     assert "workspace" in _msg(lib)
     assert gs(d, 0, 4, 1024, 256, d, None, d, d, 64, None) == INVALID
     assert gs(None, 0, 0, 1024, 256, None, None, None, None, 0, None) == OK
+
+
+def test_bf16meta_host_validation(lib):
+    """NEXT-1 entry points: the same host checks; meta replaces zmin/scale."""
+    d = ctypes.c_void_p(0x1000)
+    q = lib.actnn_quantize_bf16meta
+    assert q(d, 0, 4, 1024, 256, d, d, 1, 0, None, None, d, None, None) == INVALID
+    assert "null" in _msg(lib)
+    assert q(d, 0, 4, 1024, 128, d, d, 1, 0, None, None, d, d, None) == UNSUPPORTED
+    assert q(d, 0, 4, 1024, 256, d, d, 1, 0, None, None, d, ctypes.c_void_p(0x1002),
+             None) == INVALID
+    assert q(d, 0, 4, 1024, 256, d, d, 1, 0, None, None, ctypes.c_void_p(0x1008), d,
+             None) == UNSUPPORTED
+    assert q(None, 0, 0, 1024, 256, None, None, 1, 0, None, None, None, None, None) == OK
+    dq = lib.actnn_dequantize_bf16meta
+    assert dq(d, None, d, d, 4, 1024, 256, d, 0, None) == INVALID
+    assert dq(d, d, d, d, 4, 1024, 256, d, 5, None) == INVALID
+    assert dq(None, None, None, None, 0, 1024, 256, None, 0, None) == OK
 
 
 def test_allocate_host_validation(lib):
