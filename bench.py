@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="actnn", choices=["actnn", "reference"])
     ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--levels", default="pow2", choices=["pow2", "unit"],
+                    help="allocator widths: {1,2,4,8} (hot path) or 1..8 (the paper's unit step)")
     ap.add_argument("--meta", default="f32", choices=["f32", "bf16"],
                     help="per-group metadata: fp32 (zmin, scale) or the paper's bf16 words")
     ap.add_argument("--no-e2e", action="store_true")
@@ -210,7 +212,9 @@ def config_dict(wl, args, world, n_loc):
         "elements_per_gpu_step": E,
         "bytes_in_per_gpu_step": E * s_in,
         "G": 256,
-        "bits": ("per-sample {1,2,4,8}, avg %.2f (greedy, global over ranks)" % wl.avg_bits)
+        "bits": ("per-sample %s, avg %.2f (greedy, global over ranks)"
+                 % ("1..8 (unit step)" if getattr(args, "levels", "pow2") == "unit"
+                    else "{1,2,4,8}", wl.avg_bits))
         if wl.avg_bits is not None else f"uniform {wl.bits}",
         "parallelism": f"dp{world} (batch-sharded; all-gather of S per tensor)" if world > 1
         else "dp1",
@@ -322,7 +326,8 @@ def main():
     plan = ActivationSetPlan(xs, [W.quant_seed(t) for t in range(len(wl.acts))],
                              avg_bits=wl.avg_bits, bits=None if wl.avg_bits else wl.bits,
                              n_total=n_total, sample_base=rank * n_loc, gather=gather,
-                             meta=args.meta)
+                             meta=args.meta,
+                             level_mask=0x116 if args.levels == "pow2" else 0x1FE)
     max_numel = max(x.numel() for x in xs)
     outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(2)]
     out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
@@ -470,7 +475,8 @@ def main():
                                            "dequantize": "dequantize_fast_kernel (K4)"}[dom],
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "peak_source": peak_src, "traffic": (ncu_traffic(dom, plan.mixed)
-                            if wl.name == "c3" and args.meta == "f32" else None),
+                            if wl.name == "c3" and args.meta == "f32" and args.levels == "pow2"
+                            else None),
                 "algorithmic_bytes_per_launch": alg[dom] / launches_dom,
                 "avg_launch_us": kt[dom] * 1e3 / launches_dom,
                 "per_kernel": {k: {"ms_per_step": kt[k], "share_of_step": kt[k] / ms_step,

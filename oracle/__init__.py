@@ -71,6 +71,12 @@ def _load():
                                                         I64, P, P, ctypes.c_int]),
             "oracle_dequantize_bf16meta": (ctypes.c_int, [P, P, P, I64, I64, I32, P,
                                                           ctypes.c_int, ctypes.c_int]),
+            "oracle_relu_pack": (ctypes.c_int, [P, ctypes.c_int, I64, P, P]),
+            "oracle_relu_backward": (ctypes.c_int, [P, P, ctypes.c_int, I64, P]),
+            "oracle_maxpool2d_forward": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I64] + [I32] * 8
+                                         + [I64, I64, P, P]),
+            "oracle_maxpool2d_backward": (ctypes.c_int, [P, P, ctypes.c_int, I64, I64, I64]
+                                          + [I32] * 8 + [I64, I64, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -286,6 +292,71 @@ def dequantize_bf16meta(packed, meta, bits, N: int, D: int, G: int = 256,
     if st != 0:
         raise ValueError(f"oracle_dequantize_bf16meta failed: {st}")
     return out
+
+
+# ---------------------------------------------------------------- NEXT-4
+# Lossless contexts (P:1388-1395 ReLU, P:1406-1419 max pooling).
+
+def _dt_of(a: np.ndarray) -> int:
+    if a.dtype == np.float32:
+        return F32
+    if a.dtype == np.uint16:
+        return BF16
+    raise TypeError(a.dtype)
+
+
+def relu_pack(x: np.ndarray, want_y: bool = False):
+    """x (any shape, fp32 or bf16 bits) -> (mask u8 [ceil(E/8)], y or None)."""
+    x = np.ascontiguousarray(x)
+    E = x.size
+    mask = np.zeros((E + 7) // 8, np.uint8)
+    y = np.zeros_like(x) if want_y else None
+    st = _load().oracle_relu_pack(_ptr(x), _dt_of(x), E, _ptr(mask),
+                                  _ptr(y) if y is not None else None)
+    assert st == 0, st
+    return mask, y
+
+
+def relu_backward(mask: np.ndarray, gy: np.ndarray) -> np.ndarray:
+    gy = np.ascontiguousarray(gy)
+    mask = np.ascontiguousarray(mask, np.uint8)
+    gx = np.zeros_like(gy)
+    st = _load().oracle_relu_backward(_ptr(mask), _ptr(gy), _dt_of(gy), gy.size, _ptr(gx))
+    assert st == 0, st
+    return gx
+
+
+def pool_out(H, k, s, p, d):
+    return (H + 2 * p - d * (k - 1) - 1) // s + 1
+
+
+def maxpool2d_forward(x: np.ndarray, k, s, p=(0, 0), d=(1, 1)):
+    """x [N, C, H, W] -> (y [N, C, OH, OW], idx u8 [N, C, OH, OW])."""
+    x = np.ascontiguousarray(x)
+    N, C, H, W = x.shape
+    OH, OW = pool_out(H, k[0], s[0], p[0], d[0]), pool_out(W, k[1], s[1], p[1], d[1])
+    y = np.zeros((N, C, OH, OW), x.dtype)
+    idx = np.zeros((N, C, OH, OW), np.uint8)
+    st = _load().oracle_maxpool2d_forward(_ptr(x), _dt_of(x), N * C, H, W, k[0], k[1], s[0],
+                                          s[1], p[0], p[1], d[0], d[1], OH, OW, _ptr(y),
+                                          _ptr(idx))
+    if st != 0:
+        raise ValueError(f"oracle_maxpool2d_forward failed: {st}")
+    return y, idx
+
+
+def maxpool2d_backward(idx: np.ndarray, gy: np.ndarray, H: int, W: int, k, s, p=(0, 0),
+                       d=(1, 1)) -> np.ndarray:
+    gy = np.ascontiguousarray(gy)
+    idx = np.ascontiguousarray(idx, np.uint8)
+    N, C, OH, OW = gy.shape
+    gx = np.zeros((N, C, H, W), gy.dtype)
+    st = _load().oracle_maxpool2d_backward(_ptr(idx), _ptr(gy), _dt_of(gy), N * C, H, W, k[0],
+                                           k[1], s[0], s[1], p[0], p[1], d[0], d[1], OH, OW,
+                                           _ptr(gx))
+    if st != 0:
+        raise ValueError(f"oracle_maxpool2d_backward failed: {st}")
+    return gx
 
 
 def sharded_quantize(x: np.ndarray, k: int, avg_bits: float, seed: int,

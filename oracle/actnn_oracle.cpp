@@ -529,3 +529,117 @@ extern "C" int oracle_dequantize_bf16meta(const uint8_t* packed, const uint32_t*
     return dequantize_all(packed, nullptr, nullptr, meta, bits, N, D, G, out, out_dtype,
                           threads);
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-4: lossless contexts of a Conv-BN-ReLU-MaxPool block.                  */
+/* ------------------------------------------------------------------------- */
+
+static void store_val(void* p, int dtype, int64_t idx, float v) {
+    if (dtype == ORACLE_F32)
+        ((float*)p)[idx] = v;
+    else
+        ((uint16_t*)p)[idx] = to_bf16_rne(v);
+}
+
+/* ReLU (App. B.3): "ReLU layers are particularly simple, which
+ * have f'(x_i) = I(x_i > 0).  Therefore, ReLU layers only take a single bit per
+ * dimension to store, without any approximation."  Bit k of the LSB-first
+ * stream = (x_k > 0); y_k = x_k if x_k > 0 else +0 (when y is given). */
+extern "C" int oracle_relu_pack(const void* x, int dtype, int64_t E, uint8_t* mask, void* y) {
+    if (E < 0) return ORACLE_ERR_INVALID;
+    std::memset(mask, 0, (size_t)((E + 7) / 8));
+    for (int64_t k = 0; k < E; ++k) {
+        float v = widen(x, dtype, k);
+        bool pos = v > 0.0f;
+        if (pos) mask[k >> 3] |= (uint8_t)(1u << (k & 7));
+        if (y) store_val(y, dtype, k, pos ? v : 0.0f);
+    }
+    return ORACLE_OK;
+}
+
+/* grad_x = f'(x) * grad_y with the stored bit: grad_y where the bit is set,
+ * +0 elsewhere (exact, zero variance). */
+extern "C" int oracle_relu_backward(const uint8_t* mask, const void* gy, int dtype, int64_t E,
+                                    void* gx) {
+    if (E < 0) return ORACLE_ERR_INVALID;
+    for (int64_t k = 0; k < E; ++k) {
+        bool on = (mask[k >> 3] >> (k & 7)) & 1u;
+        store_val(gx, dtype, k, on ? widen(gy, dtype, k) : 0.0f);
+    }
+    return ORACLE_OK;
+}
+
+/* Max pooling (App. B.4) over NCHW planes, PyTorch geometry
+ * (kernel kh x kw, stride, zero-free padding, dilation, floor mode):
+ *   y[n,c,i,j] = max over the window's in-bounds taps,
+ *   k[n,c,i,j] = argmax_{Delta} (first maximum in row-major tap order), stored
+ *   as 8 bits per output location ("We use 8 bits per output location").
+ * OH/OW must equal floor((H + 2p - d(k-1) - 1)/s) + 1. */
+static int64_t pool_out(int64_t H, int k, int s, int p, int d) {
+    return (H + 2 * (int64_t)p - (int64_t)d * (k - 1) - 1) / s + 1;
+}
+
+static bool pool_ok(int64_t NC, int64_t H, int64_t W, int kh, int kw, int sh, int sw, int ph,
+                    int pw, int dh, int dw, int64_t OH, int64_t OW) {
+    if (NC < 0 || H < 1 || W < 1 || kh < 1 || kw < 1 || kh * kw > 256) return false;
+    if (sh < 1 || sw < 1 || dh < 1 || dw < 1 || ph < 0 || pw < 0) return false;
+    if (2 * ph > kh || 2 * pw > kw) return false; /* PyTorch: pad <= kernel / 2 */
+    return OH == pool_out(H, kh, sh, ph, dh) && OW == pool_out(W, kw, sw, pw, dw) && OH > 0 &&
+           OW > 0;
+}
+
+extern "C" int oracle_maxpool2d_forward(const void* x, int dtype, int64_t NC, int64_t H,
+                                        int64_t W, int kh, int kw, int sh, int sw, int ph, int pw,
+                                        int dh, int dw, int64_t OH, int64_t OW, void* y,
+                                        uint8_t* idx) {
+    if (!pool_ok(NC, H, W, kh, kw, sh, sw, ph, pw, dh, dw, OH, OW)) return ORACLE_ERR_INVALID;
+    for (int64_t p = 0; p < NC; ++p)
+        for (int64_t i = 0; i < OH; ++i)
+            for (int64_t j = 0; j < OW; ++j) {
+                bool have = false;
+                float best = 0.0f;
+                int arg = 0;
+                for (int a = 0; a < kh; ++a)
+                    for (int b = 0; b < kw; ++b) {
+                        int64_t r = i * sh - ph + (int64_t)a * dh;
+                        int64_t c = j * sw - pw + (int64_t)b * dw;
+                        if (r < 0 || r >= H || c < 0 || c >= W) continue;
+                        float v = widen(x, dtype, (p * H + r) * W + c);
+                        if (!have || v > best) {
+                            best = v;
+                            arg = a * kw + b;
+                            have = true;
+                        }
+                    }
+                int64_t o = (p * OH + i) * OW + j;
+                store_val(y, dtype, o, best);
+                idx[o] = (uint8_t)arg;
+            }
+    return ORACLE_OK;
+}
+
+/* grad_x[n,c,r,c'] = sum over output windows containing (r, c') whose stored
+ * argmax is that tap, of grad_y, accumulated in fp32 in
+ * increasing output (i, j) order from +0, then stored (bf16: RNE). */
+extern "C" int oracle_maxpool2d_backward(const uint8_t* idx, const void* gy, int dtype,
+                                         int64_t NC, int64_t H, int64_t W, int kh, int kw,
+                                         int sh, int sw, int ph, int pw, int dh, int dw,
+                                         int64_t OH, int64_t OW, void* gx) {
+    if (!pool_ok(NC, H, W, kh, kw, sh, sw, ph, pw, dh, dw, OH, OW)) return ORACLE_ERR_INVALID;
+    std::vector<float> acc((size_t)(H * W));
+    for (int64_t p = 0; p < NC; ++p) {
+        std::fill(acc.begin(), acc.end(), 0.0f);
+        for (int64_t i = 0; i < OH; ++i)
+            for (int64_t j = 0; j < OW; ++j) {
+                int64_t o = (p * OH + i) * OW + j;
+                int k = idx[o];
+                int a = k / kw, b = k % kw;
+                int64_t r = i * sh - ph + (int64_t)a * dh;
+                int64_t c = j * sw - pw + (int64_t)b * dw;
+                if (r < 0 || r >= H || c < 0 || c >= W) return ORACLE_ERR_INVARIANT;
+                acc[(size_t)(r * W + c)] += widen(gy, dtype, o);
+            }
+        for (int64_t q = 0; q < H * W; ++q) store_val(gx, dtype, p * H * W + q, acc[(size_t)q]);
+    }
+    return ORACLE_OK;
+}

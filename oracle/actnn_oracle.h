@@ -104,6 +104,26 @@ int oracle_dequantize_bf16meta(const uint8_t* packed, const uint32_t* meta,
                                const uint8_t* bits, int64_t N, int64_t D, int32_t G,
                                void* out, int out_dtype, int threads);
 
+/* NEXT-4, lossless contexts.  ReLU (App. B.3): one bit per
+ * element, bit k of the LSB-first stream = (x_k > 0); y (optional) = ReLU(x)
+ * with +0 for non-positive inputs; backward: grad_x = grad_y where the bit is
+ * set, +0 elsewhere.  E elements, mask has ceil(E/8) bytes. */
+int oracle_relu_pack(const void* x, int dtype, int64_t E, uint8_t* mask, void* y);
+int oracle_relu_backward(const uint8_t* mask, const void* gy, int dtype, int64_t E, void* gx);
+
+/* Max pooling (App. B.4) on NC planes of H x W (PyTorch
+ * geometry: kernel kh x kw <= 256 taps, stride, padding <= kernel/2,
+ * dilation, floor mode; OH/OW as PyTorch computes them).  Forward: y = window
+ * max, idx = first argmax tap (a*kw + b) in 8 bits per output location.
+ * Backward: grad_x = sum of grad_y over the windows whose argmax is that input,
+ * accumulated in fp32 in increasing output order, then stored in dtype. */
+int oracle_maxpool2d_forward(const void* x, int dtype, int64_t NC, int64_t H, int64_t W, int kh,
+                             int kw, int sh, int sw, int ph, int pw, int dh, int dw, int64_t OH,
+                             int64_t OW, void* y, uint8_t* idx);
+int oracle_maxpool2d_backward(const uint8_t* idx, const void* gy, int dtype, int64_t NC,
+                              int64_t H, int64_t W, int kh, int kw, int sh, int sw, int ph,
+                              int pw, int dh, int dw, int64_t OH, int64_t OW, void* gx);
+
 /* O10 for one group: codes from a segment and dequantised fp32 values. */
 void oracle_dequantize_group(const uint8_t* seg, int32_t len, int32_t b, float zmin,
                              float scale, uint32_t* codes, float* out);
