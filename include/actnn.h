@@ -161,6 +161,47 @@ actnn_status_t actnn_dequantize_bf16meta(const uint8_t* packed, const uint32_t* 
                                          int64_t D, int32_t G, void* out, actnn_dtype_t out_dt,
                                          void* stream);
 
+/* ---------------------------------------------------------------- NEXT-4 */
+/* Lossless contexts of a Conv-BN-ReLU-MaxPool block (the rest of the paper's
+ * per-block memory arithmetic: "2.125 bits (Conv) + 2.125 bits (BN)
+ * + 1 bit (ReLU)").  Exact: no quantisation, zero variance. */
+
+/* ReLU context (App. B.3: "ReLU layers only take a single bit per
+ * dimension to store, without any approximation").  x: E elements of dtype dt
+ * (any shape, contiguous).  mask: ceil(E/8) bytes; bit k of the LSB-first
+ * stream = (x_k > 0).  y: NULL, or E elements receiving ReLU(x) (+0 for
+ * non-positive inputs) from the same read.  Vector path when x and y are
+ * 32-byte aligned (mask 2-byte aligned for bf16); any alignment is valid. */
+actnn_status_t actnn_relu_pack(const void* x, actnn_dtype_t dt, int64_t E, uint8_t* mask,
+                               void* y, void* stream);
+
+/* ReLU backward from the mask: grad_x[k] = grad_y[k] where bit k is set, +0
+ * elsewhere (equal, bit for bit, to the full-precision ReLU gradient). */
+actnn_status_t actnn_relu_backward(const uint8_t* mask, const void* grad_y, actnn_dtype_t dt,
+                                   int64_t E, void* grad_x, void* stream);
+
+/* Max-pool context (App. B.4: "We use 8 bits per output
+ * location").  x [NC, H, W] (NCHW with NC = N*C planes), PyTorch geometry:
+ * kernel kh x kw (kh*kw <= 256, else ACTNN_ERR_UNSUPPORTED), stride sh, sw >= 1,
+ * padding ph <= kh/2, pw <= kw/2 (padded taps never win), dilation dh, dw >= 1,
+ * floor mode: OH = (H + 2 ph - dh (kh - 1) - 1) / sh + 1, OW likewise.
+ * y [NC, OH, OW] = window maximum; idx [NC, OH, OW] u8 = first argmax tap
+ * a*kw + b in row-major window order (PyTorch's tie rule). */
+actnn_status_t actnn_maxpool2d_forward(const void* x, actnn_dtype_t dt, int64_t NC, int64_t H,
+                                       int64_t W, int32_t kh, int32_t kw, int32_t sh,
+                                       int32_t sw, int32_t ph, int32_t pw, int32_t dh,
+                                       int32_t dw, void* y, uint8_t* idx, void* stream);
+
+/* Max-pool backward from the 8-bit context: grad_x[p, r, c] = sum of grad_y
+ * over the windows whose stored argmax is (r, c), accumulated in fp32 in
+ * increasing output order (bf16 output: RNE of the sum).  grad_x [NC, H, W] is
+ * fully written (zeros where no window selected the input). */
+actnn_status_t actnn_maxpool2d_backward(const uint8_t* idx, const void* grad_y,
+                                        actnn_dtype_t dt, int64_t NC, int64_t H, int64_t W,
+                                        int32_t kh, int32_t kw, int32_t sh, int32_t sw,
+                                        int32_t ph, int32_t pw, int32_t dh, int32_t dw,
+                                        void* grad_x, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

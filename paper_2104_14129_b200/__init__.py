@@ -9,5 +9,6 @@ if the CUDA library or a GPU is missing.
 """
 from .api import (  # noqa: F401
     ActnnError, Packed, abi_version, allocate_bits, compress, decompress, dequantize,
-    group_stats, library_path, packed_bytes, quantize, uniform_bits,
+    group_stats, library_path, maxpool2d, maxpool2d_backward, packed_bytes, quantize,
+    relu_backward, relu_pack, uniform_bits,
 )

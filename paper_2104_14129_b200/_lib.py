@@ -39,6 +39,12 @@ SIGNATURES = {
                                                P, P, P, P, P]),
     "actnn_dequantize_bf16meta": (ctypes.c_int, [P, P, P, P, I64, I64, I32, P, ctypes.c_int,
                                                  P]),
+    "actnn_relu_pack": (ctypes.c_int, [P, ctypes.c_int, I64, P, P, P]),
+    "actnn_relu_backward": (ctypes.c_int, [P, P, ctypes.c_int, I64, P, P]),
+    "actnn_maxpool2d_forward": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I64] + [I32] * 8
+                                + [P, P, P]),
+    "actnn_maxpool2d_backward": (ctypes.c_int, [P, P, ctypes.c_int, I64, I64, I64] + [I32] * 8
+                                 + [P, P]),
 }
 
 

@@ -251,3 +251,68 @@ def compress(x: torch.Tensor, seed: int, bits: Optional[int] = None,
 
 def decompress(p: Packed, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     return dequantize(p, out)
+
+
+# --------------------------------------------------------------------- NEXT-4
+# Lossless contexts (P:1388-1395 ReLU 1-bit mask; P:1406-1419 max-pool argmax).
+
+def relu_pack(x: torch.Tensor, want_y: bool = False):
+    """ReLU context: (mask u8 [ceil(E/8)], y = ReLU(x) or None), one read of x."""
+    x = x.contiguous()
+    if not x.is_cuda:
+        raise ActnnError(-1, "relu_pack needs a CUDA tensor")
+    E = x.numel()
+    mask = torch.empty((E + 7) // 8, dtype=torch.uint8, device=x.device)
+    y = torch.empty_like(x) if want_y else None
+    _lib.check(_lib.load().actnn_relu_pack(_ptr(x), _dtype_code(x.dtype), E, _ptr(mask), _ptr(y),
+                                           _stream(x.device)))
+    return mask, y
+
+
+def relu_backward(mask: torch.Tensor, grad_y: torch.Tensor) -> torch.Tensor:
+    grad_y = grad_y.contiguous()
+    gx = torch.empty_like(grad_y)
+    _lib.check(_lib.load().actnn_relu_backward(_ptr(mask), _ptr(grad_y),
+                                               _dtype_code(grad_y.dtype), grad_y.numel(),
+                                               _ptr(gx), _stream(grad_y.device)))
+    return gx
+
+
+def _pair(v):
+    return (v, v) if isinstance(v, int) else tuple(v)
+
+
+def _pool_extent(H, k, s, p, d):
+    return (H + 2 * p - d * (k - 1) - 1) // s + 1
+
+
+def maxpool2d(x: torch.Tensor, kernel, stride=None, padding=0, dilation=1):
+    """Max pooling with its 8-bit argmax context: (y, idx u8), x [N, C, H, W]."""
+    k = _pair(kernel)
+    s = _pair(stride if stride is not None else kernel)
+    p, d = _pair(padding), _pair(dilation)
+    x = x.contiguous()
+    if not x.is_cuda:
+        raise ActnnError(-1, "maxpool2d needs a CUDA tensor")
+    N, C, H, W = x.shape
+    OH, OW = _pool_extent(H, k[0], s[0], p[0], d[0]), _pool_extent(W, k[1], s[1], p[1], d[1])
+    y = torch.empty((N, C, OH, OW), dtype=x.dtype, device=x.device)
+    idx = torch.empty((N, C, OH, OW), dtype=torch.uint8, device=x.device)
+    _lib.check(_lib.load().actnn_maxpool2d_forward(
+        _ptr(x), _dtype_code(x.dtype), N * C, H, W, k[0], k[1], s[0], s[1], p[0], p[1], d[0],
+        d[1], _ptr(y), _ptr(idx), _stream(x.device)))
+    return y, idx
+
+
+def maxpool2d_backward(idx: torch.Tensor, grad_y: torch.Tensor, H: int, W: int, kernel,
+                       stride=None, padding=0, dilation=1) -> torch.Tensor:
+    k = _pair(kernel)
+    s = _pair(stride if stride is not None else kernel)
+    p, d = _pair(padding), _pair(dilation)
+    grad_y = grad_y.contiguous()
+    N, C = grad_y.shape[:2]
+    gx = torch.empty((N, C, H, W), dtype=grad_y.dtype, device=grad_y.device)
+    _lib.check(_lib.load().actnn_maxpool2d_backward(
+        _ptr(idx), _ptr(grad_y), _dtype_code(grad_y.dtype), N * C, H, W, k[0], k[1], s[0], s[1],
+        p[0], p[1], d[0], d[1], _ptr(gx), _stream(grad_y.device)))
+    return gx

@@ -352,4 +352,108 @@ actnn_status_t actnn_dequantize_bf16meta(const uint8_t* packed, const uint32_t* 
                            N, D, G, out, out_dt, stream);
 }
 
+// ------------------------------------------------------------ NEXT-4 contexts
+actnn_status_t actnn_relu_pack(const void* x, actnn_dtype_t dt, int64_t E, uint8_t* mask,
+                               void* y, void* stream) {
+    if (!dtype_ok(dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)dt);
+    if (E < 0) return fail(ACTNN_ERR_INVALID, "actnn_relu_pack: negative E");
+    if (E == 0) return ACTNN_OK;
+    if (!x || !mask) return fail(ACTNN_ERR_INVALID, "actnn_relu_pack: null pointer");
+    const size_t es = dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(x, es) || (y && !aligned(y, es)))
+        return fail(ACTNN_ERR_INVALID, "actnn_relu_pack: misaligned pointer");
+    ReluArgs a{x, y, mask, E, (int)dt};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_relu_pack(a, s), "actnn_relu_pack", s);
+}
+
+actnn_status_t actnn_relu_backward(const uint8_t* mask, const void* grad_y, actnn_dtype_t dt,
+                                   int64_t E, void* grad_x, void* stream) {
+    if (!dtype_ok(dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)dt);
+    if (E < 0) return fail(ACTNN_ERR_INVALID, "actnn_relu_backward: negative E");
+    if (E == 0) return ACTNN_OK;
+    if (!mask || !grad_y || !grad_x)
+        return fail(ACTNN_ERR_INVALID, "actnn_relu_backward: null pointer");
+    const size_t es = dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(grad_y, es) || !aligned(grad_x, es))
+        return fail(ACTNN_ERR_INVALID, "actnn_relu_backward: misaligned pointer");
+    ReluArgs a{grad_y, grad_x, const_cast<uint8_t*>(mask), E, (int)dt};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_relu_backward(a, s), "actnn_relu_backward", s);
+}
+
+static int64_t pool_extent(int64_t H, int k, int s, int p, int d) {
+    return (H + 2 * (int64_t)p - (int64_t)d * (k - 1) - 1) / s + 1;
+}
+
+static actnn_status_t pool_args(const char* fn, actnn_dtype_t dt, int64_t NC, int64_t H,
+                                int64_t W, int32_t kh, int32_t kw, int32_t sh, int32_t sw,
+                                int32_t ph, int32_t pw, int32_t dh, int32_t dw, PoolArgs* a) {
+    if (!dtype_ok(dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)dt);
+    if (NC < 0 || H < 1 || W < 1 || kh < 1 || kw < 1 || sh < 1 || sw < 1 || dh < 1 || dw < 1 ||
+        ph < 0 || pw < 0 || 2 * ph > kh || 2 * pw > kw)
+        return fail(ACTNN_ERR_INVALID, "%s: invalid pooling geometry", fn);
+    if (kh * kw > 256)
+        return fail(ACTNN_ERR_UNSUPPORTED, "%s: %d taps do not fit the 8-bit index", fn,
+                    kh * kw);
+    a->dt = (int)dt;
+    a->NC = NC;
+    a->H = H;
+    a->W = W;
+    a->OH = pool_extent(H, kh, sh, ph, dh);
+    a->OW = pool_extent(W, kw, sw, pw, dw);
+    if (a->OH < 1 || a->OW < 1) return fail(ACTNN_ERR_INVALID, "%s: empty output", fn);
+    a->kh = kh;
+    a->kw = kw;
+    a->sh = sh;
+    a->sw = sw;
+    a->ph = ph;
+    a->pw = pw;
+    a->dh = dh;
+    a->dw = dw;
+    return ACTNN_OK;
+}
+
+actnn_status_t actnn_maxpool2d_forward(const void* x, actnn_dtype_t dt, int64_t NC, int64_t H,
+                                       int64_t W, int32_t kh, int32_t kw, int32_t sh,
+                                       int32_t sw, int32_t ph, int32_t pw, int32_t dh,
+                                       int32_t dw, void* y, uint8_t* idx, void* stream) {
+    PoolArgs a;
+    actnn_status_t st =
+        pool_args("actnn_maxpool2d_forward", dt, NC, H, W, kh, kw, sh, sw, ph, pw, dh, dw, &a);
+    if (st) return st;
+    if (NC == 0) return ACTNN_OK;
+    if (!x || !y || !idx) return fail(ACTNN_ERR_INVALID, "actnn_maxpool2d_forward: null pointer");
+    const size_t es = dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(x, es) || !aligned(y, es))
+        return fail(ACTNN_ERR_INVALID, "actnn_maxpool2d_forward: misaligned pointer");
+    a.in = x;
+    a.out = y;
+    a.idx = idx;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_maxpool2d(a, false, s), "actnn_maxpool2d_forward", s);
+}
+
+actnn_status_t actnn_maxpool2d_backward(const uint8_t* idx, const void* grad_y,
+                                        actnn_dtype_t dt, int64_t NC, int64_t H, int64_t W,
+                                        int32_t kh, int32_t kw, int32_t sh, int32_t sw,
+                                        int32_t ph, int32_t pw, int32_t dh, int32_t dw,
+                                        void* grad_x, void* stream) {
+    PoolArgs a;
+    actnn_status_t st =
+        pool_args("actnn_maxpool2d_backward", dt, NC, H, W, kh, kw, sh, sw, ph, pw, dh, dw, &a);
+    if (st) return st;
+    if (NC == 0) return ACTNN_OK;
+    if (!idx || !grad_y || !grad_x)
+        return fail(ACTNN_ERR_INVALID, "actnn_maxpool2d_backward: null pointer");
+    const size_t es = dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(grad_y, es) || !aligned(grad_x, es))
+        return fail(ACTNN_ERR_INVALID, "actnn_maxpool2d_backward: misaligned pointer");
+    a.in = grad_y;
+    a.out = grad_x;
+    a.idx = const_cast<uint8_t*>(idx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_maxpool2d(a, true, s), "actnn_maxpool2d_backward", s);
+}
+
 }  // extern "C"

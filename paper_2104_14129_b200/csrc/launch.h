@@ -61,6 +61,31 @@ struct AllocArgs {
     int64_t* off;
 };
 
+// NEXT-4 contexts.  ReLU pack: x -> mask (+ y if non-null); backward: x = grad_y,
+// y = grad_x, mask read.
+struct ReluArgs {
+    const void* x;
+    void* y;
+    uint8_t* mask;
+    int64_t E;
+    int dt;
+};
+
+// max pool 2d: forward in = x, out = y, idx written; backward in = grad_y,
+// out = grad_x, idx read.
+struct PoolArgs {
+    const void* in;
+    void* out;
+    uint8_t* idx;
+    int dt;
+    int64_t NC, H, W, OH, OW;
+    int kh, kw, sh, sw, ph, pw, dh, dw;
+};
+
+cudaError_t launch_relu_pack(const ReluArgs& a, cudaStream_t s);
+cudaError_t launch_relu_backward(const ReluArgs& a, cudaStream_t s);
+cudaError_t launch_maxpool2d(const PoolArgs& a, bool backward, cudaStream_t s);
+
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
 cudaError_t launch_quantize_ws(const QuantArgs& a, cudaStream_t s);  // mixed-mode fast path
 cudaError_t launch_dequantize(const DequantArgs& a, cudaStream_t s);

@@ -19,7 +19,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = _lib.header_symbols()
-    assert len(names) == 11
+    assert len(names) == 15
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_lib.SIGNATURES)
@@ -101,6 +101,27 @@ def test_bf16meta_host_validation(lib):
     assert dq(d, None, d, d, 4, 1024, 256, d, 0, None) == INVALID
     assert dq(d, d, d, d, 4, 1024, 256, d, 5, None) == INVALID
     assert dq(None, None, None, None, 0, 1024, 256, None, 0, None) == OK
+
+
+def test_contexts_host_validation(lib):
+    """NEXT-4 entry points: host checks (geometry, the 256-tap limit of the
+    8-bit index, null pointers, empty problems)."""
+    d = ctypes.c_void_p(0x1000)
+    assert lib.actnn_relu_pack(d, 0, -1, d, None, None) == INVALID
+    assert lib.actnn_relu_pack(None, 0, 10, d, None, None) == INVALID
+    assert lib.actnn_relu_pack(None, 0, 0, None, None, None) == OK
+    assert lib.actnn_relu_pack(ctypes.c_void_p(0x1002), 0, 10, d, None, None) == INVALID
+    assert lib.actnn_relu_backward(d, None, 1, 10, d, None) == INVALID
+    fw, bw = lib.actnn_maxpool2d_forward, lib.actnn_maxpool2d_backward
+    geo = (3, 3, 2, 2, 1, 1, 1, 1)
+    assert fw(d, 0, 4, 112, 112, *geo, None, d, None) == INVALID
+    assert fw(d, 0, 4, 112, 112, 17, 16, 1, 1, 0, 0, 1, 1, d, d, None) == UNSUPPORTED
+    assert "8-bit" in _msg(lib)
+    assert fw(d, 0, 4, 112, 112, 3, 3, 0, 2, 1, 1, 1, 1, d, d, None) == INVALID  # stride 0
+    assert fw(d, 0, 4, 112, 112, 3, 3, 2, 2, 2, 1, 1, 1, d, d, None) == INVALID  # pad > k/2
+    assert fw(d, 0, 4, 2, 2, 5, 5, 1, 1, 0, 0, 1, 1, d, d, None) == INVALID      # empty output
+    assert fw(None, 0, 0, 112, 112, *geo, None, None, None) == OK
+    assert bw(None, d, 0, 4, 112, 112, *geo, d, None) == INVALID
 
 
 def test_allocate_host_validation(lib):
