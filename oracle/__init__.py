@@ -77,6 +77,13 @@ def _load():
                                          + [I64, I64, P, P]),
             "oracle_maxpool2d_backward": (ctypes.c_int, [P, P, ctypes.c_int, I64, I64, I64]
                                           + [I32] * 8 + [I64, I64, P]),
+            "oracle_grad_sqnorm": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I32, P]),
+            "oracle_gradmag_ema": (ctypes.c_int, [P, I64, ctypes.c_double, P]),
+            "oracle_gradmag_gather": (ctypes.c_int, [P, I64, P, I64, P]),
+            "oracle_gradmag_scatter": (ctypes.c_int, [P, I64, P, P, I64]),
+            "oracle_allocate_layers": (ctypes.c_int, [P, P, P, P, I64, I64, I64, U32, P, P]),
+            "oracle_objective_layers": (ctypes.c_double, [P, P, P, I64, I64, P]),
+            "oracle_allocate_layers_dp": (ctypes.c_double, [P, P, P, P, I64, I64, I64, U32, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -383,3 +390,94 @@ def sharded_quantize(x: np.ndarray, k: int, avg_bits: float, seed: int,
         packed, zmin, scale, _ = quantize(x[sl], bits[sl], seed, r * n_loc, G, threads)
         out.append((packed, zmin, scale, bits[sl]))
     return out
+
+
+# ---------------------------------------------------------------- NEXT-3
+def grad_sqnorm(g: np.ndarray, G: int = 256) -> np.ndarray:
+    """O14: per-sample ||grad_n||^2 (fp64 [N]) of g [N, D] (fp32 or bf16 bits)."""
+    g, dt = _as_x(g)
+    N, D = g.shape
+    out = np.zeros(N, np.float64)
+    st = _load().oracle_grad_sqnorm(_ptr(g), dt, N, D, G, _ptr(out))
+    assert st == 0, st
+    return out
+
+
+def gradmag_ema(obs: np.ndarray, m: float, rho: float = 0.9) -> float:
+    """O15: one moving-average update m <- rho m + (1 - rho) mean(obs)."""
+    obs = np.ascontiguousarray(obs, np.float64)
+    mm = np.array([m], np.float64)
+    st = _load().oracle_gradmag_ema(_ptr(obs), len(obs), float(rho), _ptr(mm))
+    if st != 0:
+        raise ValueError(f"oracle_gradmag_ema failed: {st}")
+    return float(mm[0])
+
+
+def gradmag_gather(table: np.ndarray, ids: np.ndarray) -> np.ndarray:
+    """O16: est[n] = table[ids[n]] (the stale estimate from the last epoch)."""
+    table = np.ascontiguousarray(table, np.float64)
+    ids = np.ascontiguousarray(ids, np.int64)
+    est = np.zeros(len(ids), np.float64)
+    st = _load().oracle_gradmag_gather(_ptr(table), len(table), _ptr(ids), len(ids), _ptr(est))
+    if st != 0:
+        raise ValueError(f"oracle_gradmag_gather failed: {st}")
+    return est
+
+
+def gradmag_scatter(table: np.ndarray, ids: np.ndarray, obs: np.ndarray) -> np.ndarray:
+    """O16: table[ids[n]] = obs[n]; returns the updated copy."""
+    table = np.array(table, np.float64)
+    ids = np.ascontiguousarray(ids, np.int64)
+    obs = np.ascontiguousarray(obs, np.float64)
+    st = _load().oracle_gradmag_scatter(_ptr(table), len(table), _ptr(ids), _ptr(obs), len(ids))
+    if st != 0:
+        raise ValueError(f"oracle_gradmag_scatter failed: {st}")
+    return table
+
+
+def _opt(a, dtype=np.float64):
+    if a is None:
+        return None, None
+    a = np.ascontiguousarray(a, dtype)
+    return a, _ptr(a)
+
+
+def allocate_layers(sens, D, b_total: int, level_mask: int = LEVELS_POW2, gscale=None,
+                    lconst=None):
+    """O17: stage-2 joint greedy.  sens/gscale [L, N], lconst [L], D [L]
+    -> (bits [L, N] u8, budgets [L] i64).  Raises ValueError when infeasible."""
+    sens = np.ascontiguousarray(sens, np.float64)
+    L, N = sens.shape
+    Da = np.ascontiguousarray(D, np.int64)
+    gs, gsp = _opt(gscale)
+    lc, lcp = _opt(lconst)
+    bits = np.zeros((L, N), np.uint8)
+    budgets = np.zeros(L, np.int64)
+    st = _load().oracle_allocate_layers(_ptr(sens), gsp, lcp, _ptr(Da), L, N, int(b_total),
+                                        level_mask, _ptr(bits), _ptr(budgets))
+    if st != 0:
+        raise ValueError(f"oracle_allocate_layers failed: {st}")
+    return bits, budgets
+
+
+def objective_layers(sens, bits, gscale=None, lconst=None) -> float:
+    sens = np.ascontiguousarray(sens, np.float64)
+    L, N = sens.shape
+    bits = np.ascontiguousarray(bits, np.uint8)
+    gs, gsp = _opt(gscale)
+    lc, lcp = _opt(lconst)
+    return float(_load().oracle_objective_layers(_ptr(sens), gsp, lcp, L, N, _ptr(bits)))
+
+
+def allocate_layers_dp(sens, D, b_total: int, level_mask: int = LEVELS_POW2, gscale=None,
+                       lconst=None):
+    """Exact knapsack DP of Eq. 8 over all layers (tiny instances)."""
+    sens = np.ascontiguousarray(sens, np.float64)
+    L, N = sens.shape
+    Da = np.ascontiguousarray(D, np.int64)
+    gs, gsp = _opt(gscale)
+    lc, lcp = _opt(lconst)
+    bits = np.zeros((L, N), np.uint8)
+    obj = _load().oracle_allocate_layers_dp(_ptr(sens), gsp, lcp, _ptr(Da), L, N, int(b_total),
+                                            level_mask, _ptr(bits))
+    return obj, bits

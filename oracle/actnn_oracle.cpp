@@ -643,3 +643,224 @@ extern "C" int oracle_maxpool2d_backward(const uint8_t* idx, const void* gy, int
     }
     return ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------ NEXT-3 */
+/* Run-time adaptation beyond stage 1: the gradient-magnitude
+ * factor of the sensitivity, its two estimators, and the stage-2 per-layer
+ * allocation.  DESIGN readings 22-26. */
+
+/* Canonical sum of K fp64 terms (the O11 order, DESIGN reading 11): chunks of
+ * 32 consecutive terms (zero padded), xor butterfly o = 16..1 inside a chunk,
+ * chunk totals added in order starting from +0. */
+static double canonical_sum(const double* t, int64_t K) {
+    double s = 0.0;
+    for (int64_t c = 0; c * 32 < K; ++c) {
+        double v[32], u[32];
+        for (int l = 0; l < 32; ++l) v[l] = (c * 32 + l < K) ? t[c * 32 + l] : 0.0;
+        for (int o = 16; o >= 1; o >>= 1) {
+            for (int l = 0; l < 32; ++l) u[l] = v[l] + v[l ^ o];
+            for (int l = 0; l < 32; ++l) v[l] = u[l];
+        }
+        s = s + v[0];
+    }
+    return s;
+}
+
+/* O14 (the ||grad_n||^2 factor of w_n): per-sample squared
+ * L2 norm of a gradient tensor g [N, D] (fp32 or bf16), fp64.  Reading 22: the
+ * group of G elements is split into 32 lanes of G/32 consecutive elements;
+ * lane l's term is the in-order fp64 sum of its squares (each square exact);
+ * the 32 lane terms are combined by the xor butterfly o = 16..1 (elements past
+ * D count as 0); the group totals are then summed in the canonical O11 order. */
+extern "C" int oracle_grad_sqnorm(const void* g, int dtype, int64_t N, int64_t D, int32_t G,
+                                  double* out) {
+    if (N < 0 || D < 0 || G < 32 || G % 32) return ORACLE_ERR_INVALID;
+    const int64_t ng = ceil_div(D, G);
+    const int per = G / 32;
+    std::vector<double> q((size_t)ng);
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t i = 0; i < ng; ++i) {
+            double v[32], u[32];
+            for (int l = 0; l < 32; ++l) {
+                double a = 0.0;
+                for (int k = 0; k < per; ++k) {
+                    int64_t d = i * G + (int64_t)l * per + k;
+                    double x = d < D ? (double)widen(g, dtype, n * D + d) : 0.0;
+                    a = a + x * x;
+                }
+                v[l] = a;
+            }
+            for (int o = 16; o >= 1; o >>= 1) {
+                for (int l = 0; l < 32; ++l) u[l] = v[l] + v[l ^ o];
+                for (int l = 0; l < 32; ++l) v[l] = u[l];
+            }
+            q[(size_t)i] = v[0];
+        }
+        out[n] = canonical_sum(q.data(), ng);
+    }
+    return ORACLE_OK;
+}
+
+/* O15 ("the moving average of gradient magnitude across samples"; S:369,
+ * S:372-373): m <- RN(rho * m) + RN(RN(1 - rho) * mean), mean = RN(S / N) with
+ * S the canonical sum of the N observations.  N == 0 leaves m unchanged. */
+extern "C" int oracle_gradmag_ema(const double* obs, int64_t N, double rho, double* m) {
+    if (N < 0 || !(rho >= 0.0 && rho <= 1.0)) return ORACLE_ERR_INVALID;
+    if (N == 0) return ORACLE_OK;
+    const double mean = canonical_sum(obs, N) / (double)N;
+    const double a = rho * *m;
+    const double b = (1.0 - rho) * mean;
+    *m = a + b;
+    return ORACLE_OK;
+}
+
+/* O16 ("the stale gradient magnitude in the last epoch"): a table
+ * indexed by dataset sample id.  gather: est[n] = table[ids[n]] (cold start =
+ * the caller's initial fill, 1.0 in SPEC S:371); scatter: table[ids[n]] =
+ * obs[n] (ids within one batch are distinct). */
+extern "C" int oracle_gradmag_gather(const double* table, int64_t T, const int64_t* ids,
+                                     int64_t N, double* est) {
+    for (int64_t n = 0; n < N; ++n) {
+        if (ids[n] < 0 || ids[n] >= T) return ORACLE_ERR_INVALID;
+        est[n] = table[ids[n]];
+    }
+    return ORACLE_OK;
+}
+
+extern "C" int oracle_gradmag_scatter(double* table, int64_t T, const int64_t* ids,
+                                      const double* obs, int64_t N) {
+    for (int64_t n = 0; n < N; ++n) {
+        if (ids[n] < 0 || ids[n] >= T) return ORACLE_ERR_INVALID;
+        table[ids[n]] = obs[n];
+    }
+    return ORACLE_OK;
+}
+
+/* Sensitivity of one (layer, sample) (P:547 w_n = G/6 ||grad_n||^2 ||R_n||^2;
+ * App. B per-layer constants): reading 23,
+ * w = RN(RN(sens * gscale) * lconst), absent factors = 1 (not multiplied). */
+static double sens_weight(const double* sens, const double* gscale, const double* lconst,
+                          int64_t l, int64_t N, int64_t n) {
+    double w = sens[l * N + n];
+    if (gscale) w = w * gscale[l * N + n];
+    if (lconst) w = w * lconst[l];
+    return w;
+}
+
+/* O17 (P:560 stage 2, Prob. 8 over all layers; P:566 greedy;
+ * S:332-335): joint greedy over every (layer l, sample n).  All
+ * start at the widest allowed width; the move of (l, n) from level c to c+1
+ * frees D_l * (L_c - L_{c+1}) bits and has key RN(RN(w_ln * slope_c) / D_l)
+ * (variance increase per freed bit, reading 24); moves are applied in
+ * ascending (key, l, n, c) order from a binary heap until
+ * sum_l D_l sum_n b_ln <= b_total.  budgets[l] = sum_n b_ln (P:560
+ * "b^(l) <- sum_n b_n^(l)").  bits [L*N] layer-major. */
+extern "C" int oracle_allocate_layers(const double* sens, const double* gscale,
+                                      const double* lconst, const int64_t* D, int64_t L,
+                                      int64_t N, int64_t b_total, uint32_t level_mask,
+                                      uint8_t* bits, int64_t* budgets) {
+    int Lv[8];
+    int m = mask_levels(level_mask, Lv);
+    if (m < 1 || L < 0 || N < 0) return ORACLE_ERR_INVALID;
+    int64_t total = 0, floor_bits = 0;
+    for (int64_t l = 0; l < L; ++l) {
+        if (D[l] < 1) return ORACLE_ERR_INVALID;
+        total += D[l] * N * (int64_t)Lv[0];
+        floor_bits += D[l] * N * (int64_t)Lv[m - 1];
+    }
+    if (b_total < floor_bits) return ORACLE_ERR_BUDGET;
+    double slope[8];
+    for (int c = 0; c + 1 < m; ++c)
+        slope[c] = (inv_B2(Lv[c + 1]) - inv_B2(Lv[c])) / (double)(Lv[c] - Lv[c + 1]);
+    std::vector<int> lvl((size_t)(L * N), 0);
+    typedef std::tuple<double, int64_t, int64_t, int> Move; /* (key, l, n, c) */
+    std::priority_queue<Move, std::vector<Move>, std::greater<Move>> heap;
+    auto key = [&](int64_t l, int64_t n, int c) {
+        const double w = sens_weight(sens, gscale, lconst, l, N, n);
+        return (w * slope[c]) / (double)D[l];
+    };
+    if (m > 1)
+        for (int64_t l = 0; l < L; ++l)
+            for (int64_t n = 0; n < N; ++n) heap.push(Move(key(l, n, 0), l, n, 0));
+    while (total > b_total) {
+        Move mv = heap.top();
+        heap.pop();
+        const int64_t l = std::get<1>(mv), n = std::get<2>(mv);
+        const int c = std::get<3>(mv);
+        lvl[(size_t)(l * N + n)] = c + 1;
+        total -= D[l] * (int64_t)(Lv[c] - Lv[c + 1]);
+        if (c + 2 < m) heap.push(Move(key(l, n, c + 1), l, n, c + 1));
+    }
+    for (int64_t l = 0; l < L; ++l) {
+        int64_t s = 0;
+        for (int64_t n = 0; n < N; ++n) {
+            const int b = Lv[lvl[(size_t)(l * N + n)]];
+            bits[l * N + n] = (uint8_t)b;
+            s += b;
+        }
+        budgets[l] = s;
+    }
+    return ORACLE_OK;
+}
+
+/* Eq. 8 objective over all layers: sum_l sum_n w_ln / (2^b_ln - 1)^2. */
+extern "C" double oracle_objective_layers(const double* sens, const double* gscale,
+                                          const double* lconst, int64_t L, int64_t N,
+                                          const uint8_t* bits) {
+    double s = 0.0;
+    for (int64_t l = 0; l < L; ++l)
+        for (int64_t n = 0; n < N; ++n) {
+            const double B = (double)((1 << bits[l * N + n]) - 1);
+            s += sens_weight(sens, gscale, lconst, l, N, n) / (B * B);
+        }
+    return s;
+}
+
+/* Exact minimiser of Eq. 8 over all layers under sum_l D_l sum_n b_ln <=
+ * b_total ("solved exactly by dynamic programming"), a knapsack DP over
+ * (item, bits used); test pin only, tiny instances (L*N*b_total <= 2e6). */
+extern "C" double oracle_allocate_layers_dp(const double* sens, const double* gscale,
+                                            const double* lconst, const int64_t* D, int64_t L,
+                                            int64_t N, int64_t b_total, uint32_t level_mask,
+                                            uint8_t* bits) {
+    int Lv[8];
+    int m = mask_levels(level_mask, Lv);
+    const int64_t K = L * N;
+    if (m < 1 || K < 0 || b_total < 0 || K * (b_total + 1) > 2000000) return -1.0;
+    const double INF = HUGE_VAL;
+    std::vector<std::vector<double>> dp((size_t)K + 1, std::vector<double>((size_t)b_total + 1, INF));
+    std::vector<std::vector<int8_t>> ch((size_t)K + 1, std::vector<int8_t>((size_t)b_total + 1, -1));
+    dp[0][0] = 0.0;
+    for (int64_t k = 0; k < K; ++k) {
+        const int64_t l = k / N, n = k % N;
+        const double w = sens_weight(sens, gscale, lconst, l, N, n);
+        for (int64_t u = 0; u <= b_total; ++u) {
+            if (dp[(size_t)k][(size_t)u] == INF) continue;
+            for (int c = 0; c < m; ++c) {
+                const int64_t v = u + D[l] * Lv[c];
+                if (v > b_total) continue;
+                const double B = (double)((1 << Lv[c]) - 1);
+                const double o = dp[(size_t)k][(size_t)u] + w / (B * B);
+                if (o < dp[(size_t)k + 1][(size_t)v]) {
+                    dp[(size_t)k + 1][(size_t)v] = o;
+                    ch[(size_t)k + 1][(size_t)v] = (int8_t)c;
+                }
+            }
+        }
+    }
+    int64_t best_u = -1;
+    double best = INF;
+    for (int64_t u = 0; u <= b_total; ++u)
+        if (dp[(size_t)K][(size_t)u] < best) {
+            best = dp[(size_t)K][(size_t)u];
+            best_u = u;
+        }
+    if (best_u < 0) return -1.0;
+    for (int64_t k = K, u = best_u; k > 0; --k) {
+        const int c = ch[(size_t)k][(size_t)u];
+        const int64_t l = (k - 1) / N;
+        bits[k - 1] = (uint8_t)Lv[c];
+        u -= D[l] * Lv[c];
+    }
+    return best;
+}

@@ -124,6 +124,28 @@ int oracle_maxpool2d_backward(const uint8_t* idx, const void* gy, int dtype, int
                               int64_t H, int64_t W, int kh, int kw, int sh, int sw, int ph,
                               int pw, int dh, int dw, int64_t OH, int64_t OW, void* gx);
 
+/* NEXT-3, run-time adaptation.  O14: per-sample ||grad_n||^2 of a
+ * gradient tensor [N, D] in fp64 (lane terms of G/32 consecutive squares in
+ * order, xor butterfly over the 32 lanes per group, group totals in the O11
+ * order).  O15: moving average m <- rho m + (1 - rho) mean(obs).  O16: stale
+ * per-sample table gather / scatter.  O17: stage-2 joint greedy over all
+ * layers (key RN(RN(w slope_c) / D_l), ties (l, n, c)), budgets[l] = sum_n b.
+ * w_ln = RN(RN(sens * gscale) * lconst), absent factors skipped. */
+int oracle_grad_sqnorm(const void* g, int dtype, int64_t N, int64_t D, int32_t G, double* out);
+int oracle_gradmag_ema(const double* obs, int64_t N, double rho, double* m);
+int oracle_gradmag_gather(const double* table, int64_t T, const int64_t* ids, int64_t N,
+                          double* est);
+int oracle_gradmag_scatter(double* table, int64_t T, const int64_t* ids, const double* obs,
+                           int64_t N);
+int oracle_allocate_layers(const double* sens, const double* gscale, const double* lconst,
+                           const int64_t* D, int64_t L, int64_t N, int64_t b_total,
+                           uint32_t level_mask, uint8_t* bits, int64_t* budgets);
+double oracle_objective_layers(const double* sens, const double* gscale, const double* lconst,
+                               int64_t L, int64_t N, const uint8_t* bits);
+double oracle_allocate_layers_dp(const double* sens, const double* gscale, const double* lconst,
+                                 const int64_t* D, int64_t L, int64_t N, int64_t b_total,
+                                 uint32_t level_mask, uint8_t* bits);
+
 /* O10 for one group: codes from a segment and dequantised fp32 values. */
 void oracle_dequantize_group(const uint8_t* seg, int32_t len, int32_t b, float zmin,
                              float scale, uint32_t* codes, float* out);
