@@ -58,6 +58,10 @@ typedef enum { ACTNN_F32 = 0, ACTNN_BF16 = 1 } actnn_dtype_t;
 /* op ids for actnn_workspace_bytes */
 #define ACTNN_OP_GROUP_STATS 0
 #define ACTNN_OP_ALLOCATE_BITS 1
+#define ACTNN_OP_GRAD_SQNORM 2
+
+/* Largest layer count of actnn_allocate_layers. */
+#define ACTNN_MAX_LAYERS 1024
 
 /* Thread-local message describing the last non-OK status of this thread. */
 const char* actnn_last_error(void);
@@ -160,6 +164,75 @@ actnn_status_t actnn_dequantize_bf16meta(const uint8_t* packed, const uint32_t* 
                                          const uint8_t* bits, const int64_t* off, int64_t N,
                                          int64_t D, int32_t G, void* out, actnn_dtype_t out_dt,
                                          void* stream);
+
+/* ---------------------------------------------------------------- NEXT-3 */
+/* Run-time adaptation: the gradient-magnitude factor of the
+ * sensitivity, its two estimators, and stage 2 of the allocation.  For a
+ * linear layer w_n = G/6 ||grad_n||^2 ||R_n||^2 (Eq. 7); other
+ * layer types differ by a per-layer constant (App. B: G K / (6 I A) for
+ * convolutions; a constant for normalisation). */
+
+/* Per-sample squared L2 norm of a gradient tensor, ||grad_n||^2, fp64,
+ * in the canonical order of DESIGN reading 22 (lane terms = in-order sums of
+ * the squares of G/32 consecutive elements, xor butterfly over the 32 lanes of
+ * a group, group totals in the O11 order), so results are bit-identical to the
+ * oracle.  g [N, D] of dtype dt (any D; vector path when D % 256 == 0 and g is
+ * 32-byte (fp32) / 16-byte (bf16) aligned); out [N] fp64.  ws: >=
+ * actnn_workspace_bytes(ACTNN_OP_GRAD_SQNORM, N, D, G) bytes, 8-byte aligned,
+ * zero-filled before its first use and left zero by every call (a completion
+ * ticket, as for actnn_group_stats); one workspace per stream.  One launch. */
+actnn_status_t actnn_grad_sqnorm(const void* g, actnn_dtype_t dt, int64_t N, int64_t D,
+                                 int32_t G, double* out, void* ws, size_t ws_bytes,
+                                 void* stream);
+
+/* Moving-average estimator ("the moving average of gradient magnitude
+ * across samples"): *m <- RN(rho * m) + RN(RN(1 - rho) * mean), mean =
+ * RN(S / N) with S the canonical (O11-order) sum of obs[0..N).  obs [N] fp64
+ * (e.g. the actnn_grad_sqnorm output of this step), m: one fp64 in device
+ * memory (the caller's state, initialised e.g. to 1.0).  rho in [0, 1]
+ * (else ACTNN_ERR_INVALID).  N == 0: no launch, m unchanged.  One launch. */
+actnn_status_t actnn_gradmag_ema(const double* obs, int64_t N, double rho, double* m,
+                                 void* stream);
+
+/* Stale estimator ("the stale gradient magnitude in the last epoch";
+ * S:369): a table [T] fp64 indexed by dataset sample id, owned and initialised
+ * by the caller (1.0 = cold start).  gather: est[n] = table[ids[n]];
+ * scatter: table[ids[n]] = obs[n].  ids [N] i64 must lie in [0, T) and be
+ * distinct within one scatter (device data, not validated).  One launch each. */
+actnn_status_t actnn_gradmag_gather(const double* table, int64_t T, const int64_t* ids,
+                                    int64_t N, double* est, void* stream);
+actnn_status_t actnn_gradmag_scatter(double* table, int64_t T, const int64_t* ids,
+                                     const double* obs, int64_t N, void* stream);
+
+/* Workspace bytes of actnn_allocate_layers for L layers of N samples. */
+size_t actnn_allocate_layers_ws_bytes(int64_t L, int64_t N, uint32_t level_mask);
+
+/* Stage 2 of the run-time adaptation ("After finishing the back
+ * propagation, ActNN solves Prob. (8) again for all the layers together, and
+ * sets b^(l) <- sum_n b_n^(l)"), with the paper's greedy over every
+ * (layer l, sample n): all start at the widest allowed width; the move of
+ * (l, n) from L_c to L_{c+1} frees D_l (L_c - L_{c+1}) bits and has key
+ * RN(RN(w_ln slope_c) / D_l) (variance increase per freed bit, DESIGN reading
+ * 24), w_ln = RN(RN(sens * gscale) * lconst) (absent factors skipped, reading
+ * 23); moves apply in ascending (key, l, n, c) order until
+ * sum_l D_l sum_n b_ln <= b_total.  Bit-identical to the oracle's heap.
+ *   sens [L*N] fp64 (layer-major; actnn_group_stats outputs of every layer),
+ *   gscale [L*N] fp64 or NULL (gradient estimates), lconst [L] fp64 or NULL
+ *   (per-layer constants), all finite and >= 0;
+ *   D_host [L] HOST array of per-sample feature dimensions D_l (1 <= D_l <= 2^24);
+ *   L in 0..ACTNN_MAX_LAYERS (else ACTNN_ERR_UNSUPPORTED), L*N*(levels-1) <= 2^31;
+ *   b_total: total bits; ACTNN_ERR_BUDGET when below sum_l D_l N min-width;
+ *   bits [L*N] u8 output; budgets [L] i64 output: b^(l) = sum_n b_ln, the
+ *   stage-1 budget of layer l for the next iteration (actnn_allocate_bits);
+ *   ws: >= actnn_allocate_layers_ws_bytes(L, N, level_mask) bytes, 256-byte
+ *   aligned, zero-filled before its first use and left in that state by every
+ *   call; one workspace per stream.
+ * One cooperative launch (one CTA per SM, grid-wide barriers). */
+actnn_status_t actnn_allocate_layers(const double* sens, const double* gscale,
+                                     const double* lconst, const int64_t* D_host, int64_t L,
+                                     int64_t N, int64_t b_total, uint32_t level_mask,
+                                     uint8_t* bits, int64_t* budgets, void* ws, size_t ws_bytes,
+                                     void* stream);
 
 /* ---------------------------------------------------------------- NEXT-4 */
 /* Lossless contexts of a Conv-BN-ReLU-MaxPool block (the rest of the paper's

@@ -8,7 +8,8 @@ argument marshalling only.  There is no CPU fallback: every entry point raises
 if the CUDA library or a GPU is missing.
 """
 from .api import (  # noqa: F401
-    ActnnError, Packed, abi_version, allocate_bits, compress, decompress, dequantize,
+    ActnnError, LayerAllocator, Packed, abi_version, allocate_bits, allocate_layers, compress,
+    decompress, dequantize, grad_sqnorm, gradmag_ema, gradmag_gather, gradmag_scatter,
     group_stats, library_path, maxpool2d, maxpool2d_backward, packed_bytes, quantize,
     relu_backward, relu_pack, uniform_bits,
 )

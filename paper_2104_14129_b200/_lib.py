@@ -45,6 +45,12 @@ SIGNATURES = {
                                 + [P, P, P]),
     "actnn_maxpool2d_backward": (ctypes.c_int, [P, P, ctypes.c_int, I64, I64, I64] + [I32] * 8
                                  + [P, P]),
+    "actnn_grad_sqnorm": (ctypes.c_int, [P, ctypes.c_int, I64, I64, I32, P, P, SIZE, P]),
+    "actnn_gradmag_ema": (ctypes.c_int, [P, I64, ctypes.c_double, P, P]),
+    "actnn_gradmag_gather": (ctypes.c_int, [P, I64, P, I64, P, P]),
+    "actnn_gradmag_scatter": (ctypes.c_int, [P, I64, P, P, I64, P]),
+    "actnn_allocate_layers_ws_bytes": (SIZE, [I64, I64, U32]),
+    "actnn_allocate_layers": (ctypes.c_int, [P, P, P, P, I64, I64, I64, U32, P, P, P, SIZE, P]),
 }
 
 

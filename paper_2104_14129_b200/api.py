@@ -27,6 +27,7 @@ F32, BF16 = 0, 1
 LEVELS_POW2 = (1 << 1) | (1 << 2) | (1 << 4) | (1 << 8)
 LEVELS_UNIT = 0x1FE
 OP_GROUP_STATS = 0
+OP_GRAD_SQNORM = 2
 
 
 def library_path() -> str:
@@ -316,3 +317,86 @@ def maxpool2d_backward(idx: torch.Tensor, grad_y: torch.Tensor, H: int, W: int, 
         _ptr(idx), _ptr(grad_y), _dtype_code(grad_y.dtype), N * C, H, W, k[0], k[1], s[0], s[1],
         p[0], p[1], d[0], d[1], _ptr(gx), _stream(grad_y.device)))
     return gx
+
+
+# --------------------------------------------------------------------- NEXT-3
+# Run-time adaptation: gradient-magnitude factor, its estimators,
+# stage-2 per-layer allocation.
+
+def grad_sqnorm(grad: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Per-sample ||grad_n||^2 (fp64 [N]) of a gradient tensor [N, ...]."""
+    g2 = _as_2d(grad)
+    N, D = g2.shape
+    dev = g2.device
+    out = out if out is not None else torch.empty(N, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    wsb = int(lib.actnn_workspace_bytes(OP_GRAD_SQNORM, N, D, G))
+    ws = torch.zeros(max(wsb, 8), dtype=torch.uint8, device=dev)
+    _lib.check(lib.actnn_grad_sqnorm(_ptr(g2), _dtype_code(g2.dtype), N, D, G, _ptr(out),
+                                     _ptr(ws), ws.numel(), _stream(dev)))
+    return out
+
+
+def gradmag_ema(obs: torch.Tensor, m: torch.Tensor, rho: float = 0.9) -> torch.Tensor:
+    """Moving average across samples: m (fp64 [1], device) updated in place."""
+    if obs.dtype != torch.float64 or m.dtype != torch.float64 or not obs.is_cuda:
+        raise ActnnError(-1, "gradmag_ema needs CUDA fp64 tensors")
+    obs = obs.contiguous()
+    _lib.check(_lib.load().actnn_gradmag_ema(_ptr(obs), obs.numel(), float(rho), _ptr(m),
+                                             _stream(obs.device)))
+    return m
+
+
+def gradmag_gather(table: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
+    """Stale estimator: est[n] = table[ids[n]]."""
+    ids = ids.contiguous()
+    est = torch.empty(ids.numel(), dtype=torch.float64, device=table.device)
+    _lib.check(_lib.load().actnn_gradmag_gather(_ptr(table), table.numel(), _ptr(ids),
+                                                ids.numel(), _ptr(est), _stream(table.device)))
+    return est
+
+
+def gradmag_scatter(table: torch.Tensor, ids: torch.Tensor, obs: torch.Tensor) -> torch.Tensor:
+    """Stale estimator update: table[ids[n]] = obs[n] (in place)."""
+    ids, obs = ids.contiguous(), obs.contiguous()
+    _lib.check(_lib.load().actnn_gradmag_scatter(_ptr(table), table.numel(), _ptr(ids),
+                                                 _ptr(obs), ids.numel(), _stream(table.device)))
+    return table
+
+
+class LayerAllocator:
+    """Stage 2 with a persistent zero-initialised workspace for L
+    layers of N samples: ``__call__(sens [L, N], b_total)`` -> (bits [L, N] u8,
+    budgets [L] i64), on the device in one cooperative launch."""
+
+    def __init__(self, D, N: int, device, level_mask: int = LEVELS_POW2):
+        self.D = [int(d) for d in D]
+        self.L, self.N = len(self.D), int(N)
+        self.level_mask = level_mask
+        self.dev = torch.device(device)
+        lib = _lib.load()
+        wsb = int(lib.actnn_allocate_layers_ws_bytes(self.L, self.N, level_mask))
+        self.ws = torch.zeros(max(wsb, 256), dtype=torch.uint8, device=self.dev)
+        self._D_host = (ctypes.c_int64 * max(self.L, 1))(*self.D)
+
+    def __call__(self, sens: torch.Tensor, b_total: int, gscale: Optional[torch.Tensor] = None,
+                 lconst: Optional[torch.Tensor] = None):
+        if sens.dtype != torch.float64 or not sens.is_cuda:
+            raise ActnnError(-1, "sens must be a CUDA fp64 tensor [L, N]")
+        sens = sens.contiguous()
+        gscale = gscale.contiguous() if gscale is not None else None
+        lconst = lconst.contiguous() if lconst is not None else None
+        bits = torch.empty((self.L, self.N), dtype=torch.uint8, device=self.dev)
+        budgets = torch.empty(self.L, dtype=torch.int64, device=self.dev)
+        _lib.check(_lib.load().actnn_allocate_layers(
+            _ptr(sens), _ptr(gscale), _ptr(lconst), self._D_host, self.L, self.N, int(b_total),
+            self.level_mask, _ptr(bits), _ptr(budgets), _ptr(self.ws), self.ws.numel(),
+            _stream(self.dev)))
+        return bits, budgets
+
+
+def allocate_layers(sens: torch.Tensor, D, b_total: int, level_mask: int = LEVELS_POW2,
+                    gscale: Optional[torch.Tensor] = None, lconst: Optional[torch.Tensor] = None):
+    """One-shot stage-2 allocation (a fresh workspace per call)."""
+    L, N = sens.shape
+    return LayerAllocator(D, N, sens.device, level_mask)(sens, b_total, gscale, lconst)

@@ -110,7 +110,8 @@ int actnn_abi_version(void) { return ACTNN_ABI_VERSION; }
 
 size_t actnn_workspace_bytes(int op, int64_t N, int64_t D, int32_t G) {
     if (N <= 0 || D <= 0 || G <= 0) return 0;
-    if (op == ACTNN_OP_GROUP_STATS) return (size_t)(N * ceil_div(ceil_div(D, G), 32)) * 8 + 8;
+    if (op == ACTNN_OP_GROUP_STATS || op == ACTNN_OP_GRAD_SQNORM)
+        return (size_t)(N * ceil_div(ceil_div(D, G), 32)) * 8 + 8;
     return 0;
 }
 
@@ -350,6 +351,146 @@ actnn_status_t actnn_dequantize_bf16meta(const uint8_t* packed, const uint32_t* 
         return fail(ACTNN_ERR_INVALID, "actnn_dequantize_bf16meta: null pointer");
     return dequantize_impl("actnn_dequantize_bf16meta", packed, nullptr, nullptr, meta, bits, off,
                            N, D, G, out, out_dt, stream);
+}
+
+// ------------------------------------------------------------ NEXT-3 adaptation
+actnn_status_t actnn_grad_sqnorm(const void* g, actnn_dtype_t dt, int64_t N, int64_t D,
+                                 int32_t G, double* out, void* ws, size_t ws_bytes,
+                                 void* stream) {
+    actnn_status_t st = common_checks(N, D, G);
+    if (st) return st;
+    if (!dtype_ok(dt)) return fail(ACTNN_ERR_INVALID, "bad dtype %d", (int)dt);
+    if (N == 0) return ACTNN_OK;
+    if (D == 0) {  // empty rows: ||grad_n||^2 = 0
+        if (!out) return fail(ACTNN_ERR_INVALID, "actnn_grad_sqnorm: null pointer");
+        return cuda_status(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)N,
+                                           (cudaStream_t)stream), "actnn_grad_sqnorm");
+    }
+    if (!g || !out || !ws) return fail(ACTNN_ERR_INVALID, "actnn_grad_sqnorm: null pointer");
+    const size_t es = dt == ACTNN_F32 ? 4 : 2;
+    if (!aligned(g, es) || !aligned(out, 8) || !aligned(ws, 8))
+        return fail(ACTNN_ERR_INVALID, "actnn_grad_sqnorm: misaligned pointer");
+    const size_t need = actnn_workspace_bytes(ACTNN_OP_GRAD_SQNORM, N, D, G);
+    if (ws_bytes < need)
+        return fail(ACTNN_ERR_INVALID, "actnn_grad_sqnorm: workspace %zu < %zu bytes", ws_bytes,
+                    need);
+    GradArgs a;
+    a.g = g;
+    a.dt = (int)dt;
+    a.N = N;
+    a.D = D;
+    a.ng = ceil_div(D, G);
+    a.nch = ceil_div(a.ng, 32);
+    a.out = out;
+    a.T = static_cast<double*>(ws);
+    a.fast = (D % G == 0) && aligned(g, dt == ACTNN_F32 ? 32 : 16);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_grad_sqnorm(a, s), "actnn_grad_sqnorm", s);
+}
+
+actnn_status_t actnn_gradmag_ema(const double* obs, int64_t N, double rho, double* m,
+                                 void* stream) {
+    if (N < 0) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_ema: negative N");
+    if (!(rho >= 0.0 && rho <= 1.0))
+        return fail(ACTNN_ERR_INVALID, "actnn_gradmag_ema: rho outside [0, 1]");
+    if (N == 0) return ACTNN_OK;
+    if (!obs || !m) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_ema: null pointer");
+    if (!aligned(obs, 8) || !aligned(m, 8))
+        return fail(ACTNN_ERR_INVALID, "actnn_gradmag_ema: misaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_gradmag_ema(obs, N, rho, m, s), "actnn_gradmag_ema", s);
+}
+
+actnn_status_t actnn_gradmag_gather(const double* table, int64_t T, const int64_t* ids,
+                                    int64_t N, double* est, void* stream) {
+    if (N < 0 || T < 0) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_gather: negative size");
+    if (N == 0) return ACTNN_OK;
+    if (T == 0) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_gather: empty table");
+    if (!table || !ids || !est) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_gather: null pointer");
+    if (!aligned(table, 8) || !aligned(ids, 8) || !aligned(est, 8))
+        return fail(ACTNN_ERR_INVALID, "actnn_gradmag_gather: misaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_gradmag_gather(table, ids, N, est, s), "actnn_gradmag_gather", s);
+}
+
+actnn_status_t actnn_gradmag_scatter(double* table, int64_t T, const int64_t* ids,
+                                     const double* obs, int64_t N, void* stream) {
+    if (N < 0 || T < 0) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_scatter: negative size");
+    if (N == 0) return ACTNN_OK;
+    if (T == 0) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_scatter: empty table");
+    if (!table || !ids || !obs) return fail(ACTNN_ERR_INVALID, "actnn_gradmag_scatter: null pointer");
+    if (!aligned(table, 8) || !aligned(ids, 8) || !aligned(obs, 8))
+        return fail(ACTNN_ERR_INVALID, "actnn_gradmag_scatter: misaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_gradmag_scatter(table, ids, obs, N, s), "actnn_gradmag_scatter", s);
+}
+
+size_t actnn_allocate_layers_ws_bytes(int64_t L, int64_t N, uint32_t level_mask) {
+    int Lv[8], m = 0;
+    if (L < 0 || N < 0 || level_mask == 0 || (level_mask & ~0x1FEu)) return 0;
+    for (int b = 8; b >= 1; --b)
+        if (level_mask & (1u << b)) Lv[m++] = b;
+    return allocate_layers_ws_bytes(L, N, m - 1);
+}
+
+actnn_status_t actnn_allocate_layers(const double* sens, const double* gscale,
+                                     const double* lconst, const int64_t* D_host, int64_t L,
+                                     int64_t N, int64_t b_total, uint32_t level_mask,
+                                     uint8_t* bits, int64_t* budgets, void* ws, size_t ws_bytes,
+                                     void* stream) {
+    if (L < 0 || N < 0) return fail(ACTNN_ERR_INVALID, "actnn_allocate_layers: negative size");
+    if (L > ACTNN_MAX_LAYERS)
+        return fail(ACTNN_ERR_UNSUPPORTED, "actnn_allocate_layers: L=%lld > %d", (long long)L,
+                    ACTNN_MAX_LAYERS);
+    LayerAllocArgs a;
+    std::memset(&a, 0, sizeof(a));
+    actnn_status_t st = levels_from_mask(level_mask, a.Lv, &a.m);
+    if (st) return st;
+    if (L > 0 && !D_host) return fail(ACTNN_ERR_INVALID, "actnn_allocate_layers: null D_host");
+    int64_t start = 0, floor_bits = 0;
+    for (int64_t l = 0; l < L; ++l) {
+        if (D_host[l] < 1 || D_host[l] > (1ll << 24))
+            return fail(ACTNN_ERR_UNSUPPORTED, "actnn_allocate_layers: D[%lld]=%lld outside 1..2^24",
+                        (long long)l, (long long)D_host[l]);
+        start += D_host[l] * N * a.Lv[0];
+        floor_bits += D_host[l] * N * a.Lv[a.m - 1];
+    }
+    if (b_total < floor_bits)
+        return fail(ACTNN_ERR_BUDGET, "b_total %lld < sum_l D_l N %d = %lld (infeasible)",
+                    (long long)b_total, a.Lv[a.m - 1], (long long)floor_bits);
+    if (L * N * (int64_t)(a.m - 1) > (1ll << 31))
+        return fail(ACTNN_ERR_UNSUPPORTED, "actnn_allocate_layers: %lld moves > 2^31",
+                    (long long)(L * N * (a.m - 1)));
+    if (L == 0) return ACTNN_OK;
+    if (!budgets) return fail(ACTNN_ERR_INVALID, "actnn_allocate_layers: null budgets");
+    if (N == 0)
+        return cuda_status(cudaMemsetAsync(budgets, 0, sizeof(int64_t) * (size_t)L,
+                                           (cudaStream_t)stream), "actnn_allocate_layers");
+    if (!sens || !bits || !ws) return fail(ACTNN_ERR_INVALID, "actnn_allocate_layers: null pointer");
+    if (!aligned(sens, 8) || !aligned(budgets, 8) || (gscale && !aligned(gscale, 8)) ||
+        (lconst && !aligned(lconst, 8)) || !aligned(ws, 256))
+        return fail(ACTNN_ERR_INVALID, "actnn_allocate_layers: misaligned pointer");
+    if (ws_bytes < allocate_layers_ws_bytes(L, N, a.m - 1))
+        return fail(ACTNN_ERR_INVALID, "actnn_allocate_layers: workspace %zu < %zu bytes",
+                    ws_bytes, allocate_layers_ws_bytes(L, N, a.m - 1));
+    for (int c = 0; c + 1 < a.m; ++c) {
+        const double Bh = (double)((1 << a.Lv[c]) - 1), Bl = (double)((1 << a.Lv[c + 1]) - 1);
+        const double fh = 1.0 / (Bh * Bh), fl = 1.0 / (Bl * Bl);
+        a.dstep[c] = a.Lv[c] - a.Lv[c + 1];
+        a.slope[c] = (fl - fh) / (double)a.dstep[c];
+    }
+    a.sens = sens;
+    a.gscale = gscale;
+    a.lconst = lconst;
+    a.D = D_host;
+    a.L = L;
+    a.N = N;
+    a.need = start - b_total;
+    a.bits = bits;
+    a.budgets = budgets;
+    a.ws = ws;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return post_launch(launch_allocate_layers(a, s), "actnn_allocate_layers", s);
 }
 
 // ------------------------------------------------------------ NEXT-4 contexts

@@ -82,6 +82,44 @@ struct PoolArgs {
     int kh, kw, sh, sw, ph, pw, dh, dw;
 };
 
+// NEXT-3 run-time adaptation (adapt.cu)
+constexpr int kMaxLayers = 1024;
+
+struct GradArgs {
+    const void* g;
+    int dt;
+    int64_t N, D, ng, nch;
+    double* out;
+    double* T;  // workspace [N * nch] + 8-byte ticket
+    bool fast;
+};
+
+struct LayerAllocArgs {
+    const double* sens;
+    const double* gscale;
+    const double* lconst;
+    const int64_t* D;  // host [L]
+    int64_t L, N;
+    int m;          // number of levels
+    int Lv[8];      // levels, descending
+    int dstep[8];   // Lv[c] - Lv[c+1]
+    double slope[8];
+    int64_t need;   // sum_l D_l N Lv[0] - b_total
+    uint8_t* bits;
+    int64_t* budgets;
+    void* ws;
+};
+
+cudaError_t launch_grad_sqnorm(const GradArgs& a, cudaStream_t s);
+cudaError_t launch_gradmag_ema(const double* obs, int64_t N, double rho, double* m,
+                               cudaStream_t s);
+cudaError_t launch_gradmag_gather(const double* table, const int64_t* ids, int64_t N,
+                                  double* est, cudaStream_t s);
+cudaError_t launch_gradmag_scatter(double* table, const int64_t* ids, const double* obs,
+                                   int64_t N, cudaStream_t s);
+size_t allocate_layers_ws_bytes(int64_t L, int64_t N, int m_moves);
+cudaError_t launch_allocate_layers(const LayerAllocArgs& a, cudaStream_t s);
+
 cudaError_t launch_relu_pack(const ReluArgs& a, cudaStream_t s);
 cudaError_t launch_relu_backward(const ReluArgs& a, cudaStream_t s);
 cudaError_t launch_maxpool2d(const PoolArgs& a, bool backward, cudaStream_t s);

@@ -19,7 +19,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = _lib.header_symbols()
-    assert len(names) == 15
+    assert len(names) == 21
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_lib.SIGNATURES)
@@ -147,3 +147,30 @@ def test_python_binding_refuses_cpu_tensors():
     with pytest.raises(A.ActnnError):
         A.quantize(torch.zeros(4, 1024), torch.zeros(4, dtype=torch.uint8),
                    torch.zeros(5, dtype=torch.int64), 0)
+
+
+def test_adaptation_host_validation(lib):
+    """NEXT-3 entry points: documented statuses before any launch."""
+    d = ctypes.c_void_p(0x1000)
+    D3 = (ctypes.c_int64 * 3)(10, 20, 30)
+    assert lib.actnn_workspace_bytes(2, 4, 1024, 256) == 4 * 8 + 8
+    assert lib.actnn_grad_sqnorm(None, 0, 4, 1024, 256, d, d, 64, None) == INVALID
+    assert lib.actnn_grad_sqnorm(d, 0, 4, 1024, 128, d, d, 64, None) == UNSUPPORTED
+    assert lib.actnn_grad_sqnorm(d, 0, 4, 1024, 256, d, d, 8, None) == INVALID  # small ws
+    assert lib.actnn_grad_sqnorm(d, 0, 0, 1024, 256, None, None, 0, None) == OK
+    assert lib.actnn_gradmag_ema(d, 4, 1.5, d, None) == INVALID
+    assert lib.actnn_gradmag_ema(None, 0, 0.9, None, None) == OK
+    assert lib.actnn_gradmag_gather(d, 0, d, 3, d, None) == INVALID
+    assert lib.actnn_gradmag_scatter(d, 10, None, d, 3, None) == INVALID
+    assert lib.actnn_allocate_layers_ws_bytes(3, 8, 0x116) >= 3 * 8 * 3 * 8
+    assert lib.actnn_allocate_layers_ws_bytes(3, 8, 0) == 0
+    al = lib.actnn_allocate_layers
+    # infeasible: below sum_l D_l N * 1
+    assert al(d, None, None, D3, 3, 2, 119, 0x116, d, d, d, 1 << 20, None) == BUDGET
+    assert "infeasible" in _msg(lib)
+    assert al(d, None, None, D3, 2000, 2, 10 ** 9, 0x116, d, d, d, 1 << 20, None) == UNSUPPORTED
+    assert al(d, None, None, D3, 3, 2, 500, 0x3, d, d, d, 1 << 20, None) == INVALID  # mask
+    bigD = (ctypes.c_int64 * 1)(1 << 25)
+    assert al(d, None, None, bigD, 1, 2, 1 << 30, 0x116, d, d, d, 1 << 20, None) == UNSUPPORTED
+    assert al(d, None, None, D3, 3, 2, 500, 0x116, d, d, d, 16, None) == INVALID  # small ws
+    assert al(None, None, None, None, 0, 5, 0, 0x116, None, None, None, 0, None) == OK
