@@ -37,6 +37,27 @@ struct SParams {
     unsigned int* ticket;  // zero before the first call; left zero by every call
 };
 
+__device__ __forceinline__ uint4 ldg_nc_u4(const uint16_t* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint4 ldg_nc_u4(const float*) { return make_uint4(0, 0, 0, 0); }
+
+// per-half min / max of two bf16x2 words
+__device__ __forceinline__ uint32_t bmin2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
 template <typename T, bool kFast>
 __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) {
     constexpr int kU = SCfg<T>::U;
@@ -53,7 +74,30 @@ __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) 
         const int gcount = (int)min((int64_t)kChunk, p.ng - g0);
         const int gw = w * kU;  // this warp's first group within the chunk
         float myMn = 0.0f, myMx = 0.0f;
-        if (kFast) {
+        if constexpr (kFast && sizeof(T) == 2) {
+            // bf16: min and max on packed bf16x2 words (both are exact on bf16
+            // values), carried through the butterfly as one (min, -max) pair
+            uint4 q[kU];
+            const T* src = x + n * p.D + (g0 + gw) * kG + lane * 8;
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                if (gw + u < gcount) q[u] = ldg_nc_u4(src + u * kG);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (gw + u < gcount) {
+                    const uint32_t mn2 = bmin2(bmin2(q[u].x, q[u].y), bmin2(q[u].z, q[u].w));
+                    const uint32_t mx2 = bmax2(bmax2(q[u].x, q[u].y), bmax2(q[u].z, q[u].w));
+                    const uint32_t nmx2 = mx2 ^ 0x80008000u;  // -max, exact
+                    uint32_t r = bmin2(__byte_perm(mn2, nmx2, 0x5410), __byte_perm(mn2, nmx2, 0x7632));
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) r = bmin2(r, __shfl_xor_sync(kFull, r, o));
+                    if (lane == u) {
+                        myMn = __uint_as_float(r << 16);
+                        myMx = __uint_as_float((r & 0xFFFF0000u) ^ 0x80000000u);
+                    }
+                }
+            }
+        } else if (kFast) {
             float v[kU][8];
             const T* src = x + n * p.D + (g0 + gw) * kG + lane * 8;
 #pragma unroll
