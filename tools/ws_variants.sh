@@ -13,6 +13,6 @@ for v in "${VARS[@]}"; do
 done; wait
 for f in build/var/w_*.o; do
   tag=$(basename $f .o | sed s/^w_//)
-  $NV $A -shared -o build/var/libactnn_$tag.so build/abi.o build/quantize.o $f build/dequantize.o build/stats.o build/allocate.o
+  $NV $A -shared -o build/var/libactnn_$tag.so $(ls build/*.o | grep -v quantize_ws) $f
   echo "$tag $(grep -E 'Used|spill' build/var/w_$tag.txt | paste - - | grep -o 'Used [0-9]* reg\|[0-9]* bytes spill stores' | tr '\n' ' ')"
 done
