@@ -68,16 +68,30 @@ inline RoundKeys make_round_keys(uint64_t seed) {
     return rk;
 }
 
+// 32 x 32 -> 64-bit product as one IMAD.WIDE.U32 (4 FMA-heavy cycles; the
+// separate IMAD.HI + IMAD form ptxas sometimes picks costs 6).
+__device__ __forceinline__ void mulwide(uint32_t a, uint32_t m, uint32_t& hi, uint32_t& lo) {
+    uint64_t p;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(m));
+    lo = (uint32_t)p;
+    hi = (uint32_t)(p >> 32);
+}
+
 __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, const RoundKeys& rk) {
-    uint32_t c2 = 0u, c3 = 0u;
+    // round 0 with c2 = c3 = 0: the second product is 0
+    uint32_t hi0, lo0, hi1, lo1;
+    mulwide(c0, 0xD2511F53u, hi0, lo0);
+    uint32_t n0 = c1 ^ rk.k[0];
+    uint32_t n2 = hi0 ^ rk.k[1];
+    c0 = n0;
+    c1 = 0u;
+    uint32_t c2 = n2, c3 = lo0;
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint32_t lo0 = 0xD2511F53u * c0;
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c0);
-        const uint32_t lo1 = 0xCD9E8D57u * c2;
-        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
-        const uint32_t n0 = hi1 ^ c1 ^ rk.k[2 * r];
-        const uint32_t n2 = hi0 ^ c3 ^ rk.k[2 * r + 1];
+    for (int r = 1; r < 10; ++r) {
+        mulwide(c0, 0xD2511F53u, hi0, lo0);
+        mulwide(c2, 0xCD9E8D57u, hi1, lo1);
+        n0 = hi1 ^ c1 ^ rk.k[2 * r];
+        n2 = hi0 ^ c3 ^ rk.k[2 * r + 1];
         c0 = n0;
         c1 = lo1;
         c2 = n2;
@@ -127,13 +141,13 @@ __device__ __forceinline__ void load8(const uint16_t* p, float v[8]) {
                  : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
                  : "l"(p));
     // bf16 -> fp32 is exact: the bf16 bits are the high half of the fp32 bits
-    v[0] = __uint_as_float(a << 16);
+    v[0] = __uint_as_float(__byte_perm(a, 0u, 0x1044));
     v[1] = __uint_as_float(a & 0xFFFF0000u);
-    v[2] = __uint_as_float(b << 16);
+    v[2] = __uint_as_float(__byte_perm(b, 0u, 0x1044));
     v[3] = __uint_as_float(b & 0xFFFF0000u);
-    v[4] = __uint_as_float(c << 16);
+    v[4] = __uint_as_float(__byte_perm(c, 0u, 0x1044));
     v[5] = __uint_as_float(c & 0xFFFF0000u);
-    v[6] = __uint_as_float(d << 16);
+    v[6] = __uint_as_float(__byte_perm(d, 0u, 0x1044));
     v[7] = __uint_as_float(d & 0xFFFF0000u);
 }
 
@@ -235,6 +249,38 @@ __device__ __forceinline__ uint32_t sr_code(float h, float Z, float inv14, uint3
     return (__float_as_uint(t) - 0x4B400000u + r14) >> 14;
 }
 
+// Codes of one lane's 8 elements at b <= 2 (ACTNN-Q v1 O5-O7), two elements
+// per 32-bit register: t = RN(d * inv14 + 1.5 2^23) holds q = RNE(d * inv14)
+// < 2^16 in its low half (the magic's low 16 bits are zero), so one byte
+// permute gives T = q_y << 16 | q_x; adding the two 14-bit draws
+// (w & 0x3FFF3FFF) cannot carry across halves (q + r < (B + 1) 2^14 <= 2^16),
+// and bits 14.. of each half are the codes.  The codes are moved to their
+// packed positions (element j at bits [j b, (j + 1) b)) with shifts and masks
+// on the ALU pipe -- no multiply, since the FMA-heavy pipe is the one the
+// Philox IMAD.WIDEs saturate.
+template <int b>
+__device__ __forceinline__ uint32_t codes_small(const float v[8], float Z, float inv14,
+                                                const Philox4& o) {
+    // scalar FADD/FFMA: measured ~6% faster per group than the f32x2 forms
+    // (tools/cuda_checks/k3_compute.cu), which also compete with the Philox
+    // IMAD.WIDEs for the FMA-heavy pipe
+    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+    uint32_t y = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const float tx = __fmaf_rn(__fsub_rn(v[2 * p], Z), inv14, 12582912.0f);
+        const float ty = __fmaf_rn(__fsub_rn(v[2 * p + 1], Z), inv14, 12582912.0f);
+        uint32_t T = __byte_perm(__float_as_uint(tx), __float_as_uint(ty), 0x5410);
+        T += w[p] & 0x3FFF3FFFu;
+        if (b == 2)  // half 0 code -> bits 4p.., half 1 code -> bits 16 + 4p..
+            y |= (T >> (14 - 4 * p)) & (0xC000C000u >> (14 - 4 * p));
+        else  // half 0 code -> bit 2p, half 1 code -> bit 16 + 2p
+            y |= (T >> (14 - 2 * p)) & (0x40004000u >> (14 - 2 * p));
+    }
+    if (b == 2) return (y | (y >> 14)) & 0xFFFFu;
+    return (y | (y >> 15)) & 0xFFu;
+}
+
 // ACTNN-Q v1 O10: h_hat = fmaf((float)code, scale, Z); (float)code is exact
 // via the 2^23 magic (code < 2^8).
 __device__ __forceinline__ float dequant1(uint32_t code, float scale, float Z) {
@@ -302,13 +348,14 @@ __device__ __forceinline__ void lds8(const float* p, float v[8]) {
 
 __device__ __forceinline__ void lds8(const uint16_t* p, float v[8]) {
     const uint4 a = *reinterpret_cast<const uint4*>(p);
-    v[0] = __uint_as_float(a.x << 16);
+    // bits << 16 as a byte permute (ALU pipe, not an IMAD shift)
+    v[0] = __uint_as_float(__byte_perm(a.x, 0u, 0x1044));
     v[1] = __uint_as_float(a.x & 0xFFFF0000u);
-    v[2] = __uint_as_float(a.y << 16);
+    v[2] = __uint_as_float(__byte_perm(a.y, 0u, 0x1044));
     v[3] = __uint_as_float(a.y & 0xFFFF0000u);
-    v[4] = __uint_as_float(a.z << 16);
+    v[4] = __uint_as_float(__byte_perm(a.z, 0u, 0x1044));
     v[5] = __uint_as_float(a.z & 0xFFFF0000u);
-    v[6] = __uint_as_float(a.w << 16);
+    v[6] = __uint_as_float(__byte_perm(a.w, 0u, 0x1044));
     v[7] = __uint_as_float(a.w & 0xFFFF0000u);
 }
 

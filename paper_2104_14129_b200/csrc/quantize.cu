@@ -128,38 +128,7 @@ __device__ __forceinline__ void group_const_store(float mn, float mx, int b, uin
     }
 }
 
-// Codes of a lane's 8 elements for b in {1, 2}, packed LSB-first (O8) into the
-// low 8 b bits.  Pair p = elements (2p, 2p+1) uses Philox word p, whose low
-// and high 16-bit halves are the two draws (O6).  With t = bits of
-// fma(h - Z, inv14, 1.5*2^23) = 0x4B400000 + q (O5):
-//   T = t1 * 2^16 + t0 + (w & 0x3FFF3FFF) - 0x4B400000
-//     = (q0 + r0) + (q1 + r1) * 2^16       (mod 2^32; q + r < 2^16 for b <= 2)
-// so code0 = T[14, 14+b) and code1 = T[30, 30+b) (O7).  Masking those bits
-// and one IMAD.HI by a two-term constant moves code0 to bit s = 2pb and code1
-// to bit s + b of the payload; the cross terms land at bits >= 16 and are
-// masked off at the end.
-template <int b>
-__device__ __forceinline__ uint32_t codes_small(const float v[8], float Z, float inv14,
-                                                const Philox4& o) {
-    const float2 nz = make_float2(-Z, -Z);
-    const float2 iv = make_float2(inv14, inv14);
-    const float2 mg = make_float2(12582912.0f, 12582912.0f);
-    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
-    uint32_t acc = 0;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
-        const float2 t = __ffma2_rn(d, iv, mg);
-        uint32_t T = __float_as_uint(t.y) * 65536u + __float_as_uint(t.x);
-        T = T + (w[p] & 0x3FFF3FFFu) - 0x4B400000u;
-        if (b == 2) {
-            acc |= __umulhi(T & 0xC000C000u, (1u << (18 + 4 * p)) + (1u << (4 + 4 * p)));
-        } else {
-            acc |= __umulhi(T & 0x40004000u, (1u << (18 + 2 * p)) + (1u << (3 + 2 * p)));
-        }
-    }
-    return acc & ((1u << (8 * b)) - 1u);
-}
+// Codes for b in {1, 2}: codes_small (device.cuh).
 
 // Codes for b >= 3 (q up to 2^22): one code per element (scalar fp32 ops; the
 // f32x2 form of this variant miscompiled in testing).

@@ -1,7 +1,9 @@
 // quantize_ws.cu -- K3 for the mixed-precision path (gmin/gmax from K1),
 // warp-specialised.  Same bytes as quantize.cu, ACTNN-Q v1 O4-O9.
 //
-// A CTA = kCons consumer warps + 1 producer warp.  Consumer warp w walks the
+// A CTA = kCons consumer warps + kProd producer warps (each serving kCons/kProd
+// consumers; one producer warp per 8 consumers was latency-bound on its own
+// dependency chains at bf16, where a unit holds 8 groups).  Consumer warp w walks the
 // units u = (blockIdx * kCons + w) + r * nwarps (a unit = U consecutive groups
 // of one sample, 4 KB of input); it owns a ring of S shared-memory stages.
 // The producer warp, S rounds ahead of the consumers, for every consumer's
@@ -36,7 +38,7 @@ namespace {
 #define ACTNN_WS_PH 2
 #endif
 #ifndef ACTNN_WS_LAZY
-#define ACTNN_WS_LAZY -1  // -1: lazy for bf16, eager for fp32 (measured best)
+#define ACTNN_WS_LAZY -1  // -1: lazy for bf16, eager for fp32 (measured best); 2 packed-eager
 #endif
 #ifndef ACTNN_WS_MD
 #define ACTNN_WS_MD 1  // rounds of (gmin, gmax) prefetched by the producer (1-6 measured: 1 best)
@@ -44,8 +46,13 @@ namespace {
 #ifndef ACTNN_WS_MINB
 #define ACTNN_WS_MINB 2
 #endif
+#ifndef ACTNN_WS_PROD
+#define ACTNN_WS_PROD 2
+#endif
 constexpr int kCons = ACTNN_WS_CONS;      // consumer warps per CTA
-constexpr int kThreads = (kCons + 1) * 32;
+constexpr int kProd = ACTNN_WS_PROD;      // producer warps per CTA (kCons / kProd consumers each)
+constexpr int kThreads = (kCons + kProd) * 32;
+static_assert(kCons % kProd == 0 && 32 % (kCons / kProd) == 0, "producer lane split");
 constexpr int kS = ACTNN_WS_S;            // stages per consumer
 constexpr int kMD = ACTNN_WS_MD;
 constexpr int kUnitBytes = 4096;          // one TMA copy per unit
@@ -57,7 +64,13 @@ struct WS {
     static constexpr int U = kUnitBytes / (kG * (int)sizeof(T));  // groups per unit: 4 / 8
     static constexpr int SE = kUnitBytes / (int)sizeof(T);        // elements per stage
     static constexpr int PH = ACTNN_WS_PH;                          // Philox chains interleaved
-    static constexpr bool kLazy = ACTNN_WS_LAZY < 0 ? sizeof(T) == 2 : ACTNN_WS_LAZY != 0;
+    // stage consumption: 0 eager (all groups to fp32 registers, release, compute),
+    // 1 lazy (PH groups at a time, release after the last), 2 packed-eager (bf16:
+    // the raw bf16x2 words of all groups to registers -- half the registers of
+    // eager -- release, unpack per group while computing)
+    static constexpr int kMode = ACTNN_WS_LAZY < 0 ? (sizeof(T) == 2 ? 1 : 0)
+                                                   : (sizeof(T) == 4 && ACTNN_WS_LAZY == 2 ? 0
+                                                                                            : ACTNN_WS_LAZY);
 };
 
 struct __align__(16) Desc {
@@ -104,54 +117,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// hi32(a * b) + c in one IMAD.HI
-__device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t d;
-    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-
-// Codes of one lane's 8 elements at b <= 2, two elements per 32-bit register:
-// t = RN(d * inv14 + 1.5 2^23) holds q = RNE(d * inv14) < 2^16 in its low half
-// (the magic's low 16 bits are zero), so one byte permute gives
-// T = q_y << 16 | q_x; adding the two 14-bit draws (w & 0x3FFF3FFF) cannot
-// carry across halves (q + r < (B + 1) 2^14 <= 2^16), and bits 14.. of each
-// half are the codes (ACTNN-Q v1 O5-O7).  One multiply-high per pair moves the
-// two codes to their packed positions; the positions of different pairs are
-// disjoint, so the accumulation is an add.
-template <int b>
-__device__ __forceinline__ uint32_t ws_codes_small(const float v[8], float Z, float inv14,
-                                                   const Philox4& o) {
-    const float2 nz = make_float2(-Z, -Z);
-    const float2 iv = make_float2(inv14, inv14);
-    const float2 mg = make_float2(12582912.0f, 12582912.0f);
-    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
-    uint32_t acc = 0;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
-        const float2 t = __ffma2_rn(d, iv, mg);
-        uint32_t T = __byte_perm(__float_as_uint(t.x), __float_as_uint(t.y), 0x5410);
-        T += w[p] & 0x3FFF3FFFu;
-        if (b == 2)
-            acc = madhi(T & 0xC000C000u, (1u << (18 + 4 * p)) + (1u << (4 + 4 * p)), acc);
-        else
-            acc = madhi(T & 0x40004000u, (1u << (18 + 2 * p)) + (1u << (3 + 2 * p)), acc);
-    }
-    return acc & ((1u << (8 * b)) - 1u);
-}
-
 // Codes of one group at width b from its Philox draw, packed and stored
 // (ACTNN-Q v1 O5-O8; the same arithmetic as quantize.cu).
 template <int b>
 __device__ __forceinline__ void ws_store(const float v[8], float Z, float inv14,
                                          const Philox4& o, uint8_t* seg, int lane) {
     if constexpr (b == 2) {
-        const uint32_t pl = ws_codes_small<2>(v, Z, inv14, o);
+        const uint32_t pl = codes_small<2>(v, Z, inv14, o);
         const uint32_t q = __shfl_down_sync(kFull, pl, 1);
         if (!(lane & 1)) *reinterpret_cast<uint32_t*>(seg + lane * 2) = pl | (q << 16);
     } else if constexpr (b == 1) {
-        const uint32_t pl = ws_codes_small<1>(v, Z, inv14, o);
+        const uint32_t pl = codes_small<1>(v, Z, inv14, o);
         const uint32_t q1 = __shfl_down_sync(kFull, pl, 1);
         const uint32_t q2 = __shfl_down_sync(kFull, pl, 2);
         const uint32_t q3 = __shfl_down_sync(kFull, pl, 3);
@@ -360,6 +336,90 @@ __device__ __forceinline__ void ws_unit_eager(const T* st, const Desc& d, uint8_
     }
 }
 
+// bf16 packed-eager: the unit's raw words (4 per group per lane) are read from
+// the stage, the stage is released at once, and each group is unpacked to fp32
+// just before its codes are formed.
+__device__ __forceinline__ void unpack8(const uint4& a, float v[8]) {
+    v[0] = __uint_as_float(__byte_perm(a.x, 0u, 0x1044));
+    v[1] = __uint_as_float(a.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(__byte_perm(a.y, 0u, 0x1044));
+    v[3] = __uint_as_float(a.y & 0xFFFF0000u);
+    v[4] = __uint_as_float(__byte_perm(a.z, 0u, 0x1044));
+    v[5] = __uint_as_float(a.z & 0xFFFF0000u);
+    v[6] = __uint_as_float(__byte_perm(a.w, 0u, 0x1044));
+    v[7] = __uint_as_float(a.w & 0xFFFF0000u);
+}
+
+template <int b>
+__device__ __forceinline__ void ws_packed_full(const uint4 (&raw)[8], const float (&Zs)[8],
+                                               const float (&Is)[8], uint64_t blk, uint8_t* seg,
+                                               const RoundKeys& rk, int lane) {
+    constexpr int U = 8;
+    constexpr int PH = ACTNN_WS_PH;
+#pragma unroll
+    for (int h = 0; h < U; h += PH) {
+        Philox4 o[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const uint64_t c = blk + (uint64_t)((h + q) * 32);
+            o[q] = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), rk);
+        }
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            float v[8];
+            unpack8(raw[h + q], v);
+            ws_store<b>(v, Zs[h + q], Is[h + q], o[q], seg + (h + q) * 32 * b, lane);
+        }
+    }
+}
+
+__device__ __forceinline__ void ws_unit_packed(const uint16_t* st, const Desc& d, uint8_t* packed,
+                                               const RoundKeys& rk, int lane, uint64_t* empty) {
+    constexpr int U = 8;
+    const int gcount = (int)d.gcount;
+    const int b = (int)d.b;
+    uint4 raw[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+        if (k < gcount) raw[k] = *reinterpret_cast<const uint4*>(st + k * kG + lane * 8);
+    const uint64_t seg0 = d.seg, blk0 = d.blk0;
+    float Zs[U], Is[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        Zs[k] = d.Z[k];
+        Is[k] = d.inv[k];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty);
+    uint8_t* seg = packed + seg0;
+    if (gcount == U) {
+        const uint64_t blk = blk0 + (uint64_t)lane;
+        if (b == 1) return ws_packed_full<1>(raw, Zs, Is, blk, seg, rk, lane);
+        if (b == 2) return ws_packed_full<2>(raw, Zs, Is, blk, seg, rk, lane);
+        if (b == 4) return ws_packed_full<4>(raw, Zs, Is, blk, seg, rk, lane);
+        if (b == 8) return ws_packed_full<8>(raw, Zs, Is, blk, seg, rk, lane);
+    }
+    constexpr int PH = ACTNN_WS_PH;
+#pragma unroll
+    for (int h = 0; h < U; h += PH) {
+        Philox4 o[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const uint64_t blk = blk0 + (uint64_t)((h + q) * 32 + lane);
+            o[q] = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+        }
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            const int k = h + q;
+            if (k < gcount) {
+                float v[8];
+                unpack8(raw[k], v);
+                ws_store_any<0>(b, v, Zs[k], Is[k], o[q], seg + k * 32 * b, lane);
+            }
+        }
+    }
+}
+
 template <typename T, bool kCached>
 __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(const __grid_constant__ WSParams p) {
     constexpr int U = WS<T>::U;
@@ -389,14 +449,14 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
     __syncthreads();
     const uint32_t nwarps = gridDim.x * kCons;
 
-    if (w == kCons) {
+    if (w >= kCons) {
         // ------------------------------------------------------------ producer
-        // lane l serves consumer c = l / (32 / kCons) ... generalised: each step
-        // covers kCons units x U groups with 32 lanes: a lane handles groups
-        // k = (l % LPC) + t * LPC of consumer c = l / LPC, LPC = 32 / kCons.
-        constexpr int LPC = 32 / kCons;        // lanes per consumer (4)
-        constexpr int GPL = U / LPC;           // groups per lane (1 or 2)
-        const int c = lane / LPC, kl = lane % LPC;
+        // producer warp i serves consumers [i CPP, (i + 1) CPP): its lane l
+        // handles groups k = (l % LPC) + t LPC of consumer i CPP + l / LPC.
+        constexpr int CPP = kCons / kProd;           // consumers per producer warp
+        constexpr int LPC = 32 / CPP;                // lanes per consumer
+        constexpr int GPL = U > LPC ? U / LPC : 1;   // groups per lane
+        const int c = (w - kCons) * CPP + lane / LPC, kl = lane % LPC;
         uint32_t u0 = blockIdx.x * kCons + c;
         uint32_t n = u0 / p.nb, j = u0 % p.nb;
         const T* __restrict__ x = static_cast<const T*>(p.x);
@@ -506,7 +566,18 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
         mbar_wait(&full[slot], ph);
         const Desc& d = desc[slot];
         const T* st = ring + (size_t)slot * SE;
-        if constexpr (WS<T>::kLazy)
+#ifdef ACTNN_WS_DRYRUN  // diagnostics: the pipeline alone (read the stage, release, no codes)
+        if (true) {
+            const uint4 r = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(st) + lane * 16);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if ((r.x ^ r.y ^ r.z ^ r.w) == 0x12345u) p.packed[lane] = 1;
+        } else
+#endif
+        if constexpr (WS<T>::kMode == 2)
+            ws_unit_packed(reinterpret_cast<const uint16_t*>(st), d, p.packed, p.rk, lane,
+                           &empty[slot]);
+        else if constexpr (WS<T>::kMode == 1)
             ws_unit_lazy<T>(st, d, p.packed, p.rk, lane, &empty[slot]);
         else
             ws_unit_eager<T>(st, d, p.packed, p.rk, lane, &empty[slot]);

@@ -75,6 +75,53 @@ KERNEL(k_hilo, {
     b[i] = l;
 })
 
+
+// heavy-pipe interference: one IMAD.WIDE chain step plus FP work per iteration
+KERNEL(k_wide_ffma2, {
+    uint64_t p;
+    asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a[i]), "r"(0xD2511F53u));
+    float2 f = make_float2(__uint_as_float(b[i]), __uint_as_float(a[i]));
+    float2 g;
+    asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(*(uint64_t*)&g) : "l"(*(uint64_t*)&f), "l"(*(uint64_t*)&f), "l"(*(uint64_t*)&f));
+    asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(*(uint64_t*)&f) : "l"(*(uint64_t*)&g), "l"(*(uint64_t*)&g), "l"(*(uint64_t*)&g));
+    a[i] = (uint32_t)p ^ __float_as_uint(f.x);
+    b[i] = (uint32_t)(p >> 32) ^ __float_as_uint(f.y);
+})
+KERNEL(k_wide_ffma4, {
+    uint64_t p;
+    asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a[i]), "r"(0xD2511F53u));
+    float x = __uint_as_float(b[i]), y = __uint_as_float(a[i]);
+    asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(x));
+    asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(y));
+    asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(x));
+    asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(y));
+    a[i] = (uint32_t)p ^ __float_as_uint(x);
+    b[i] = (uint32_t)(p >> 32) ^ __float_as_uint(y);
+})
+KERNEL(k_wide_only, {
+    uint64_t p;
+    asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a[i]), "r"(0xD2511F53u));
+    a[i] = (uint32_t)p ^ b[i];
+    b[i] = (uint32_t)(p >> 32) ^ 0x1234u;
+})
+KERNEL(k_ffma2_only, {
+    float2 f = make_float2(__uint_as_float(b[i]), __uint_as_float(a[i]));
+    asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(*(uint64_t*)&f));
+    a[i] = __float_as_uint(f.x);
+    b[i] = __float_as_uint(f.y);
+})
+KERNEL(k_wide_prmt4, {
+    uint64_t p;
+    asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a[i]), "r"(0xD2511F53u));
+    uint32_t x = b[i], y = a[i];
+    asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(x) : "r"(y));
+    asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(y) : "r"(x));
+    asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(x) : "r"(y));
+    asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(y) : "r"(x));
+    a[i] = (uint32_t)p ^ x;
+    b[i] = (uint32_t)(p >> 32) ^ y;
+})
+
 typedef void (*KFn)(uint32_t, uint32_t, uint32_t*);
 
 int main() {
@@ -91,6 +138,9 @@ int main() {
         {"mul.lo (IMAD) +xor", k_lo, 2},          {"xor (LOP3) x2", k_lop, 2},
         {"add (IADD3)", k_add, 1},                {"fma.f32 (FFMA)", k_ffma, 1},
         {"prmt", k_prmt, 1},                      {"mul.hi+mul.lo +xor", k_hilo, 3},
+        {"wide+xor2 only", k_wide_only, 3},       {"wide + 2 FFMA2", k_wide_ffma2, 5},
+        {"wide + 4 FFMA", k_wide_ffma4, 7},       {"FFMA2 only", k_ffma2_only, 1},
+        {"wide + 4 PRMT", k_wide_prmt4, 7},
     };
     const uint32_t iters = 4096;
     for (auto& k : ks) {
