@@ -45,6 +45,8 @@ def parse():
                     help="per-group metadata: fp32 (zmin, scale) or the paper's bf16 words")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-adapt", action="store_true",
+                    help="skip the NEXT-3 side measurement (gradient norms, stage-2 allocation)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
@@ -486,6 +488,13 @@ def main():
     total_alg = sum(alg.values())
     avg_bits = [float(b.double().mean()) for b in bits_host]
 
+    # ---- NEXT-3 side measurement (not part of the step): per-sample gradient
+    # norms over every tensor of the set (the activations stand in for
+    # gradients of the same shape: same bytes, same kernel) and the stage-2
+    # joint allocation over all layers
+    adapt = None
+    if plan.mixed and world == 1 and not args.no_adapt:
+        adapt = run_adapt(A, plan, xs, wl, s_in, torch, peak, barrier)
     # ---- e2e through the public API with host buffers (per-layer pipeline)
     e2e = None
     if not args.no_e2e:
@@ -510,6 +519,8 @@ def main():
             "avg_bits_realised": sum(avg_bits) / len(avg_bits)}
     if e2e is not None:
         line["e2e"] = e2e
+    if adapt is not None:
+        line["adapt"] = adapt
     if rank == 0 and world == 1 and not args.no_cpu:
         cb, _ = cpu_sample(wl, wl.acts, args, args.cpu_seconds, W.quant_seed, torch)
         line["cpu_baseline"] = cb
@@ -518,6 +529,66 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_adapt(A, plan, xs, wl, s_in, torch, peak, barrier, reps=5):
+    """K6 over every tensor (event pair per launch) and K5 on the [L, N]
+    sensitivities of this step, timed on the current stream."""
+    outs = [torch.empty(x.shape[0], dtype=torch.float64, device=x.device) for x in xs]
+    ws = [torch.zeros(int(A._lib.load().actnn_workspace_bytes(2, x.shape[0],
+                                                             x.numel() // x.shape[0], 256)) + 8,
+                      dtype=torch.uint8, device=x.device) for x in xs]
+    lib = A._lib.load()
+    cs = torch.cuda.current_stream()
+    sp = __import__("ctypes").c_void_p(cs.cuda_stream)
+
+    def sqnorm(i):
+        x = xs[i]
+        N = x.shape[0]
+        A._lib.check(lib.actnn_grad_sqnorm(A.api._ptr(x), A.api._dtype_code(x.dtype), N,
+                                           x.numel() // N, 256, A.api._ptr(outs[i]),
+                                           A.api._ptr(ws[i]), ws[i].numel(), sp))
+
+    for i in range(len(xs)):
+        sqnorm(i)
+    barrier()
+    t_k6 = 0.0
+    for _ in range(reps):
+        for i in range(len(xs)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cs)
+            sqnorm(i)
+            b.record(cs)
+            b.synchronize()
+            t_k6 += a.elapsed_time(b)
+    t_k6 /= reps
+    nbytes = sum(x.numel() for x in xs) * s_in
+    D = [L.D for L in plan.layers]
+    N = plan.layers[0].N
+    sens = torch.stack([L.S[:N] for L in plan.layers]).contiguous()
+    gscale = torch.stack(outs).contiguous()  # ||grad_n||^2 estimates of this step
+    alloc = A.LayerAllocator(D, N, xs[0].device, plan.level_mask)
+    b_total = int(wl.avg_bits * N * sum(D))
+    alloc(sens, b_total, gscale)
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(cs)
+    for _ in range(reps):
+        bits, budgets = alloc(sens, b_total, gscale)
+    b.record(cs)
+    b.synchronize()
+    t_k5 = a.elapsed_time(b) / reps
+    used = int((budgets.cpu() * torch.tensor(D)).sum())
+    return {"grad_sqnorm": {"kernel": "grad_sqnorm_kernel (K6)", "ms_per_set": t_k6,
+                            "GBps": nbytes / (t_k6 * 1e-3) / 1e9,
+                            "frac": nbytes / (t_k6 * 1e-3) / 1e9 / peak,
+                            "launches": len(xs)},
+            "stage2": {"kernel": "allocate_layers_kernel (K5)", "us": t_k5 * 1e3,
+                       "layers": len(D), "samples": N,
+                       "moves": len(D) * N * (bin(plan.level_mask).count("1") - 1),
+                       "b_total": b_total, "bits_used": used},
+            "note": "NEXT-3 (P:553-569) side measurement, not part of the step; the "
+                    "activations stand in for same-shaped gradients"}
 
 
 def run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist, s_in,

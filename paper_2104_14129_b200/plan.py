@@ -69,6 +69,7 @@ class ActivationSetPlan:
         self.dfn = (self.lib.actnn_dequantize if meta == "f32"
                     else self.lib.actnn_dequantize_bf16meta)
         self.mixed = avg_bits is not None
+        self.level_mask = level_mask
         # k > 1: gather(S_global, S_local) fills S_global[N_total] with every
         # rank's S_n (an all-gather over NCCL: the exchange step, equivalent
         # to the all-reduce of zero-padded vectors and exact)

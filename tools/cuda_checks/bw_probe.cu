@@ -84,6 +84,43 @@ __global__ void write_stg(float* __restrict__ y, size_t n_kb) {
     for (size_t u = w; u < n_kb; u += nw) store8(y + u * 256 + lane * 8, v);
 }
 
+// STG.256 with the streaming (evict-first) hint
+__global__ void write_stg_cs(float* __restrict__ y, size_t n_kb) {
+    const int lane = threadIdx.x & 31;
+    size_t w = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+    const size_t nw = (gridDim.x * (size_t)blockDim.x) >> 5;
+    float v[8];
+    for (int j = 0; j < 8; ++j) v[j] = (float)(lane + j);
+    for (size_t u = w; u < n_kb; u += nw)
+        asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(y + u * 256 + lane * 8),
+                     "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]),
+                     "f"(v[7]) : "memory");
+}
+
+// TMA bulk store: each warp owns an KB-kilobyte shared buffer (filled once) and
+// streams it to consecutive global chunks with cp.async.bulk.global.shared::cta,
+// at most D bulk groups in flight.
+template <int KB, int D>
+__global__ void write_tma(float* __restrict__ y, size_t n_kb) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    float* buf = reinterpret_cast<float*>(smem) + (size_t)wi * KB * 256;
+    for (int i = lane; i < KB * 256; i += 32) buf[i] = (float)i;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    const size_t w = blockIdx.x * (size_t)nwb + wi, nw = (size_t)gridDim.x * nwb;
+    const size_t units = n_kb / KB;
+    if (lane == 0) {
+        for (size_t u = w; u < units; u += nw) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(y + u * KB * 256),
+                         "r"(smem_u32(buf)), "r"(KB * 1024) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(D) : "memory");
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
 template <class F>
 float time_ms(F f, int reps = 10) {
     cudaEvent_t a, b;
@@ -133,6 +170,19 @@ int main() {
     for (int bps : {2, 4, 8})
         printf("write_stg 256thr x %d/SM: %.0f GB/s\n", bps,
                gbs(time_ms([&] { write_stg<<<sms * bps, 256>>>(y, n_kb); })));
+    for (int bps : {2, 4, 8})
+        printf("write_stg_cs 256thr x %d/SM: %.0f GB/s\n", bps,
+               gbs(time_ms([&] { write_stg_cs<<<sms * bps, 256>>>(y, n_kb); })));
+#define WT(KB, D, WARPS, BPS)                                                                    \
+    {                                                                                            \
+        size_t sm = (size_t)WARPS * KB * 1024;                                                   \
+        cudaFuncSetAttribute(write_tma<KB, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                             (int)sm);                                                           \
+        printf("write_tma KB=%d depth=%d warps=%d x %d/SM: %.0f GB/s\n", KB, D, WARPS, BPS,       \
+               gbs(time_ms([&] { write_tma<KB, D><<<sms * BPS, WARPS * 32, sm>>>(y, n_kb); }))); \
+    }
+    WT(4, 2, 8, 2) WT(4, 4, 8, 2) WT(4, 8, 8, 2) WT(8, 4, 4, 2) WT(16, 4, 4, 2) WT(4, 4, 4, 4)
+    WT(2, 8, 8, 4) WT(32, 2, 2, 2)
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }

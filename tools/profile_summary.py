@@ -52,4 +52,13 @@ if os.path.exists(rep):
     open(os.path.join(dst, f"{tag}_full.txt"), "w").write(
         "# ncu --set full --clock-control none, largest C3 tensor (bn1 input, 256x64x112x112 "
         "fp32), tools/make_profiles.sh\n" + out)
+for suffix, what in (("c4_full", "largest C4 tensor (1024x64x112x112 bf16, mixed widths)"),
+                     ("adapt_full", "NEXT-3 kernels: K6 grad_sqnorm on the largest C3 (fp32) and "
+                                    "C4 (bf16) tensors, K5 stage 2 on 311 layers x 1024 samples")):
+    rep = os.path.join(src, f"{tag}_{suffix}.ncu-rep")
+    if os.path.exists(rep):
+        out = subprocess.run([sys.executable, os.path.join(root, "tools", "ncu_details.py"), rep],
+                             capture_output=True, text=True).stdout
+        open(os.path.join(dst, f"{tag}_{suffix}.txt"), "w").write(
+            f"# ncu --set full --clock-control none, {what}, tools/make_profiles.sh\n" + out)
 print(buf.getvalue())
