@@ -180,10 +180,10 @@ __device__ __forceinline__ void ws_store_any(int bw, const float v[8], float Z, 
 // is used, and the stage (data + descriptor) is released after the last
 // batch's reads -- only PH groups of data live in registers, which leaves room
 // for more consumer warps per SM (ACTNN_WS_MINB = 3, ACTNN_WS_S = 2).
-template <int b, typename T>
+template <int b, typename T, typename Rel>
 __device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_t blk,
                                              uint8_t* seg, const RoundKeys& rk, int lane,
-                                             uint64_t* empty) {
+                                             const Rel& rel) {
     constexpr int U = WS<T>::U;
     constexpr int PH = WS<T>::PH;
 #pragma unroll
@@ -198,7 +198,7 @@ __device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_
         }
         if (h + PH >= U) {
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty);
+            if (lane == 0) rel();
         }
         Philox4 o[PH];
 #pragma unroll
@@ -212,9 +212,9 @@ __device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_
     }
 }
 
-template <typename T>
+template <typename T, typename Rel>
 __device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t* packed,
-                                        const RoundKeys& rk, int lane, uint64_t* empty) {
+                                        const RoundKeys& rk, int lane, const Rel& rel) {
     constexpr int U = WS<T>::U;
     constexpr int PH = WS<T>::PH;
     const int gcount = (int)d.gcount;
@@ -223,10 +223,10 @@ __device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t
     uint8_t* seg = packed + d.seg;
     if (gcount == U) {  // the common case, at the allocator's widths {1, 2, 4, 8}
         const uint64_t blk = blk0 + (uint64_t)lane;
-        if (b == 2) return ws_lazy_full<2, T>(st, d, blk, seg, rk, lane, empty);
-        if (b == 1) return ws_lazy_full<1, T>(st, d, blk, seg, rk, lane, empty);
-        if (b == 4) return ws_lazy_full<4, T>(st, d, blk, seg, rk, lane, empty);
-        if (b == 8) return ws_lazy_full<8, T>(st, d, blk, seg, rk, lane, empty);
+        if (b == 2) return ws_lazy_full<2, T>(st, d, blk, seg, rk, lane, rel);
+        if (b == 1) return ws_lazy_full<1, T>(st, d, blk, seg, rk, lane, rel);
+        if (b == 4) return ws_lazy_full<4, T>(st, d, blk, seg, rk, lane, rel);
+        if (b == 8) return ws_lazy_full<8, T>(st, d, blk, seg, rk, lane, rel);
     }
 #pragma unroll
     for (int h = 0; h < U; h += PH) {
@@ -240,7 +240,7 @@ __device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t
         }
         if (h + PH >= U) {  // last batch: every read of the stage is issued
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty);
+            if (lane == 0) rel();
         }
         Philox4 o[PH];
 #pragma unroll
@@ -274,9 +274,9 @@ __device__ __forceinline__ void ws_full_unit(const float (&v)[U][8], const float
     }
 }
 
-template <typename T>
+template <typename T, typename Rel>
 __device__ __forceinline__ void ws_unit_eager(const T* st, const Desc& d, uint8_t* packed,
-                                        const RoundKeys& rk, int lane, uint64_t* empty) {
+                                        const RoundKeys& rk, int lane, const Rel& rel) {
     constexpr int U = WS<T>::U;
     const int gcount = (int)d.gcount;
     const int b = (int)d.b;
@@ -294,7 +294,7 @@ __device__ __forceinline__ void ws_unit_eager(const T* st, const Desc& d, uint8_
     // every lane's shared reads of this stage are issued: release it (the
     // producer's next bulk copy into it first has to fetch from HBM)
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty);
+    if (lane == 0) rel();
     uint8_t* seg = packed + seg0;
     if (gcount == U) {  // the common case, at the allocator's widths {1, 2, 4, 8}
         constexpr int PH = WS<T>::PH;
@@ -373,8 +373,9 @@ __device__ __forceinline__ void ws_packed_full(const uint4 (&raw)[8], const floa
     }
 }
 
+template <typename Rel>
 __device__ __forceinline__ void ws_unit_packed(const uint16_t* st, const Desc& d, uint8_t* packed,
-                                               const RoundKeys& rk, int lane, uint64_t* empty) {
+                                               const RoundKeys& rk, int lane, const Rel& rel) {
     constexpr int U = 8;
     const int gcount = (int)d.gcount;
     const int b = (int)d.b;
@@ -390,7 +391,7 @@ __device__ __forceinline__ void ws_unit_packed(const uint16_t* st, const Desc& d
         Is[k] = d.inv[k];
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty);
+    if (lane == 0) rel();
     uint8_t* seg = packed + seg0;
     if (gcount == U) {
         const uint64_t blk = blk0 + (uint64_t)lane;
@@ -566,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
         mbar_wait(&full[slot], ph);
         const Desc& d = desc[slot];
         const T* st = ring + (size_t)slot * SE;
+        auto rel = [&] { mbar_arrive(&empty[slot]); };
 #ifdef ACTNN_WS_DRYRUN  // diagnostics: the pipeline alone (read the stage, release, no codes)
         if (true) {
             const uint4 r = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(st) + lane * 16);
@@ -575,12 +577,11 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
         } else
 #endif
         if constexpr (WS<T>::kMode == 2)
-            ws_unit_packed(reinterpret_cast<const uint16_t*>(st), d, p.packed, p.rk, lane,
-                           &empty[slot]);
+            ws_unit_packed(reinterpret_cast<const uint16_t*>(st), d, p.packed, p.rk, lane, rel);
         else if constexpr (WS<T>::kMode == 1)
-            ws_unit_lazy<T>(st, d, p.packed, p.rk, lane, &empty[slot]);
+            ws_unit_lazy<T>(st, d, p.packed, p.rk, lane, rel);
         else
-            ws_unit_eager<T>(st, d, p.packed, p.rk, lane, &empty[slot]);
+            ws_unit_eager<T>(st, d, p.packed, p.rk, lane, rel);
         if (++s == kS) {
             s = 0;
             ph ^= 1u;

@@ -20,9 +20,14 @@ namespace {
 
 // groups per warp per chunk: 4 (fp32: 4 KB in flight per warp) or 8 (bf16:
 // also 4 KB); a CTA has 32 / U warps so that a chunk is 32 groups.
+#ifndef ACTNN_K1_U16
+#define ACTNN_K1_U16 4
+#endif
 template <typename T>
 struct SCfg {
-    static constexpr int U = 4;  // (8 for bf16 measured slower: 96 regs, 20 warps/SM)
+    // groups per warp: 4 (4 KB fp32 / 2 KB bf16 in flight); 8 bf16 groups per
+    // warp measured 8% slower on the largest C4 tensor (fewer CTAs per SM)
+    static constexpr int U = sizeof(T) == 2 ? ACTNN_K1_U16 : 4;
     static constexpr int Block = (kChunk / U) * 32;
 };
 constexpr unsigned kFull = 0xffffffffu;

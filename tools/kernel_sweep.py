@@ -41,7 +41,9 @@ for li in layers:
                               scale=p.scale))
     td = t(lambda: A.dequantize(p, out=out))
     ts = t(lambda: A.group_stats(x))
+    gn = A.grad_sqnorm(x)
+    tg = t(lambda: A.grad_sqnorm(x, out=gn))
     res[f"L{li}"] = {"MB": round(nbytes / 1e6, 1), "stats_us": round(ts, 1),
-                     "quant_us": round(tq, 1), "dequant_us": round(td, 1),
+                     "quant_us": round(tq, 1), "dequant_us": round(td, 1), "sqnorm_us": round(tg, 1),
                      "quant_TBps_in": round(nbytes / tq / 1e6, 2)}
 print(json.dumps(res))
