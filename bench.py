@@ -298,10 +298,18 @@ def main():
     # one process per GPU; ACTNN_DIST_BACKEND=gloo is a test mode in which
     # several ranks may share a GPU (NCCL refuses duplicate devices)
     backend = os.environ.get("ACTNN_DIST_BACKEND", "nccl")
+    # ACTNN_FORCE_DIST=1: the multi-rank code path (process group, all-gather of
+    # S, graph capture of the collectives) even at world size 1 -- a test mode
+    dist_on = world > 1 or os.environ.get("ACTNN_FORCE_DIST") == "1"
+    if dist_on:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", str(world))
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if dist_on:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -313,13 +321,26 @@ def main():
     s_in = 4 if wl.dtype == "f32" else 2
     tdt = torch.float32 if wl.dtype == "f32" else torch.bfloat16
 
-    # resident inputs (generated on the device, seeded per tensor and rank)
+    # resident inputs must fit: C5 (batch 4096, 365.8 GB of bf16 activations in
+    # total) needs >= 4 GPUs; smaller N would have to stream tensors from host
+    need = n_loc * sum(a.D for a in wl.acts) * s_in * 1.1
+    free = torch.cuda.mem_get_info(dev)[0]
+    if need > free:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world,
+                              "config": config_dict(wl, args, world, n_loc),
+                              "error": "resident inputs need %.1f GB per GPU, %.1f GB free: "
+                                       "run %s on more GPUs" % (need / 1e9, free / 1e9,
+                                                                wl.name.upper())}), flush=True)
+        if dist_on:
+            dist.destroy_process_group()
+        return 1
     xs = []
     for t, a in enumerate(wl.acts):
         xs.append(W.synth_activation(a, n_loc, t + 100_000 * rank, wl.dtype, dev))
     torch.cuda.synchronize()
     gather = None
-    if world > 1:
+    if dist_on:
         def gather(S, S_loc):
             if backend == "nccl":
                 dist.all_gather_into_tensor(S, S_loc)
@@ -366,7 +387,7 @@ def main():
             plan.decompress_layer(i, outs[i & 1], out_dt, sp, ev[nl + i])
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         torch.cuda.synchronize()
 
@@ -380,15 +401,26 @@ def main():
     # exactly the work of an eager step.  At N>1 the step holds a collective
     # (all-gather of S); it stays eager there.
     graph = None
+    graph_error = None
     if args.graph is None:
-        args.graph = world == 1
+        # N > 1: the NCCL all-gathers are captured too (tests/test_gpu_parity.py
+        # checks replay == eager through a real NCCL group); ACTNN_DIST_GRAPH=0
+        # keeps the multi-GPU step eager
+        args.graph = not dist_on or (backend == "nccl"
+                                    and os.environ.get("ACTNN_DIST_GRAPH", "1") != "0")
     if args.graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            plan.compress_all(stream, side, alloc_s)
-            plan.decompress_all(outs, out_dt, [stream, aux])
-        graph.replay()
-        barrier()
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                plan.compress_all(stream, side, alloc_s)
+                plan.decompress_all(outs, out_dt, [stream, aux])
+            graph.replay()
+            barrier()
+        except Exception as e:  # fall back to the eager schedule
+            graph, graph_error, args.graph = None, f"{type(e).__name__}: {e}"[:200], False
+            torch.cuda.synchronize()
+            barrier()
+    if graph is not None:
         eager_step = step
 
         def step(ev=None):  # noqa: F811
@@ -406,7 +438,7 @@ def main():
         e1.record()
         barrier()
     ms = e0.elapsed_time(e1)
-    if world > 1:
+    if dist_on:
         tt = torch.tensor([ms], dtype=torch.float64,
                           device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -506,7 +538,8 @@ def main():
             "higher_is_better": True, "scaling": "weak" if args.config != "c5" else "strong",
             "vs_baseline": None, "dtype": wl.dtype,
             "data": "synthetic (seeded ResNet-shaped activations generated on the GPU)",
-            "config": config_dict(wl, args, world, n_loc),
+            "config": dict(config_dict(wl, args, world, n_loc),
+                           **({"graph_error": graph_error} if graph_error else {})),
             # phases of the pipelined schedule (events at the boundary; rank-local)
             "compress_GBps": world * E_loc * s_in / (t_comp * 1e-3) / 1e9,
             "decompress_GBps": world * E_loc * s_in / (t_decomp * 1e-3) / 1e9,
@@ -526,7 +559,7 @@ def main():
         line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return 0
 
