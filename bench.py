@@ -410,12 +410,20 @@ def main():
                                     and os.environ.get("ACTNN_DIST_GRAPH", "1") != "0")
     if args.graph:
         try:
+            ref_bits = [L.bits.clone() for L in plan.layers] if dist_on else None
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
                 plan.compress_all(stream, side, alloc_s)
                 plan.decompress_all(outs, out_dt, [stream, aux])
+            if dist_on:  # the replay must redo the exchange: clear S, compare the widths
+                for L in plan.layers:
+                    L.S.zero_()
+                torch.cuda.synchronize()
             graph.replay()
             barrier()
+            if dist_on and not all(torch.equal(L.bits, r) for L, r in zip(plan.layers, ref_bits)):
+                raise RuntimeError("graph replay did not reproduce the eager widths "
+                                   "(captured all-gather not replayed)")
         except Exception as e:  # fall back to the eager schedule
             graph, graph_error, args.graph = None, f"{type(e).__name__}: {e}"[:200], False
             torch.cuda.synchronize()

@@ -17,12 +17,21 @@
 namespace actnn {
 namespace {
 
-constexpr int kU = 4;
+#ifndef ACTNN_DQ_U
+#define ACTNN_DQ_U 4
+#endif
+constexpr int kU = ACTNN_DQ_U;  // groups per unit
 constexpr int kWarps = 8;
 constexpr int kBlock = kWarps * 32;
-constexpr int kS = 4;                     // stages per warp
+#ifndef ACTNN_DQ_S
+#define ACTNN_DQ_S 4
+#endif
+#ifndef ACTNN_DQ_MINB
+#define ACTNN_DQ_MINB 3
+#endif
+constexpr int kS = ACTNN_DQ_S;            // stages per warp
 constexpr int kPay = kU * 32 * 8;         // payload bytes at the widest (b = 8)
-constexpr int kStage = kPay + 32;         // + 4 zero points + 4 scales
+constexpr int kStage = kPay + 8 * kU;     // + kU zero points + kU scales
 constexpr int kNCap = 2048;
 constexpr size_t kSmem = (size_t)kWarps * kS * kStage + (size_t)kWarps * kS * 8 + kNCap +
                          4 * (kNCap + 1);
@@ -126,7 +135,7 @@ __device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount,
 // kB16: NEXT-1 bf16 metadata words (Z', R'): lane u < 4 widens group u's word
 // and computes scale = RN(R' / B) once, the unit's lanes get it by shuffle.
 template <typename TO, bool kCached, bool kMeta, bool kB16>
-__global__ void __launch_bounds__(kBlock, 3)
+__global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
     dequantize_fast_kernel(const __grid_constant__ DParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
@@ -171,13 +180,13 @@ __global__ void __launch_bounds__(kBlock, 3)
         uint8_t* dst = ring + s * kStage;
         if (kMeta && kB16) {
             const uint32_t g = pn * p.ng + pj * kU;
-            mbar_expect_tx(&bars[s], bytes + 16);
-            bulk_g2s(dst + kPay, p.meta + g, 16, &bars[s]);
+            mbar_expect_tx(&bars[s], bytes + 4 * kU);
+            bulk_g2s(dst + kPay, p.meta + g, 4 * kU, &bars[s]);
         } else if (kMeta) {
             const uint32_t g = pn * p.ng + pj * kU;
-            mbar_expect_tx(&bars[s], bytes + 32);
-            bulk_g2s(dst + kPay, p.zmin + g, 16, &bars[s]);
-            bulk_g2s(dst + kPay + 16, p.scale + g, 16, &bars[s]);
+            mbar_expect_tx(&bars[s], bytes + 8 * kU);
+            bulk_g2s(dst + kPay, p.zmin + g, 4 * kU, &bars[s]);
+            bulk_g2s(dst + kPay + 4 * kU, p.scale + g, 4 * kU, &bars[s]);
         } else {
             mbar_expect_tx(&bars[s], bytes);
         }
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(kBlock, 3)
             }
         } else {
             const float* zp = kMeta ? reinterpret_cast<const float*>(st + kPay) : p.zmin + g;
-            const float* sp = kMeta ? reinterpret_cast<const float*>(st + kPay + 16) : p.scale + g;
+            const float* sp = kMeta ? reinterpret_cast<const float*>(st + kPay + 4 * kU) : p.scale + g;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 zq[u] = u < gcount ? zp[u] : 0.0f;

@@ -398,40 +398,12 @@ def test_compress_sharded_one_rank_nccl(A, W):
 def test_pipelined_step_graph_with_nccl_gather(A, W):
     """The pipelined step with the NCCL exchange of S (1-rank group) captured in
     a CUDA graph: replays equal the eager step byte for byte (the multi-GPU
-    bench replays this graph)."""
-    import torch.distributed as dist
-    from paper_2104_14129_b200.plan import ActivationSetPlan
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ["MASTER_PORT"] = "29541"
-    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
-    try:
-        acts = [W.resnet_activation_set(50)[i] for i in (3, 12, 40)]
-        xs = [W.synth_activation(a, 8, i, "f32", DEV) for i, a in enumerate(acts)]
-
-        def gather(S, S_loc):
-            dist.all_gather_into_tensor(S, S_loc)
-
-        plan = ActivationSetPlan(xs, [11, 12, 13], avg_bits=2.0, n_total=8, gather=gather)
-        outs = [torch.empty(max(x.numel() for x in xs), device=DEV) for _ in range(2)]
-        main, side, al, aux = (torch.cuda.Stream(), torch.cuda.Stream(),
-                               torch.cuda.Stream(priority=-1), torch.cuda.Stream())
-        with torch.cuda.stream(main):
-            plan.compress_all(main, side, al)
-            plan.decompress_all(outs, A.api.F32, [main, aux])
-        torch.cuda.synchronize()
-        ref = [host(L.packed).copy() for L in plan.layers]
-        ref_out = host(outs[0]).copy()
-        for L in plan.layers:
-            L.packed.zero_()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=main):
-            plan.compress_all(main, side, al)
-            plan.decompress_all(outs, A.api.F32, [main, aux])
-        for _ in range(3):
-            g.replay()
-        torch.cuda.synchronize()
-        for L, r in zip(plan.layers, ref):
-            assert np.array_equal(host(L.packed), r)
-        assert np.array_equal(host(outs[0]), ref_out)
-    finally:
-        dist.destroy_process_group()
+    bench replays this graph).  Runs in a fresh process: a process group
+    created after another one was destroyed in the same process does not
+    replay its captured collectives (observed in this suite)."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "..", "tools",
+                                                     "graph_nccl_check.py")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
