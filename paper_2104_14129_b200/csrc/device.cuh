@@ -326,6 +326,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Wait with a suspend-time hint: the thread sleeps until the phase completes
+// (or the hint, in ns, expires) instead of re-polling, so waiting warps do not
+// take issue slots from the working ones.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity,
+                                                uint32_t hint_ns = 100000u) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"

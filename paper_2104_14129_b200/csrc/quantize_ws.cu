@@ -46,6 +46,12 @@ namespace {
 #ifndef ACTNN_WS_MINB
 #define ACTNN_WS_MINB 2
 #endif
+#ifndef ACTNN_WS_PWAIT
+#define ACTNN_WS_PWAIT mbar_wait_sleep  // producer: sleep on the empty barrier
+#endif
+#ifndef ACTNN_WS_CWAIT
+#define ACTNN_WS_CWAIT mbar_wait
+#endif
 #ifndef ACTNN_WS_PROD
 #define ACTNN_WS_PROD 2
 #endif
@@ -499,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
             const int s = (int)(r % kS);
             const int slot = c * kS + s;
             if (r >= (uint32_t)kS && valid && kl == 0)
-                mbar_wait(&empty[slot], ((r / kS) - 1) & 1);
+                ACTNN_WS_PWAIT(&empty[slot], ((r / kS) - 1) & 1);
             __syncwarp();
             const uint32_t gi = j * U;
             const int gcount = (int)min((uint32_t)U, p.ng - gi);
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
     uint32_t ph = 0;
     while (n < p.N) {
         const int slot = w * kS + s;
-        mbar_wait(&full[slot], ph);
+        ACTNN_WS_CWAIT(&full[slot], ph);
         const Desc& d = desc[slot];
         const T* st = ring + (size_t)slot * SE;
         auto rel = [&] { mbar_arrive(&empty[slot]); };
