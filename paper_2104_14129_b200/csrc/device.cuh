@@ -107,6 +107,32 @@ __device__ __forceinline__ uint32_t rnd14(const Philox4& o, int j) {
 }
 
 // ------------------------------------------------------------- warp helpers
+// per-half min / max of two bf16x2 words
+__device__ __forceinline__ uint32_t bmin2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+// Group (min, max) of 8 bf16 values per lane (four bf16x2 words) over the
+// warp: min and -max travel as one bf16x2 pair through the butterfly (both
+// exact on bf16 values); returns them widened to fp32.
+__device__ __forceinline__ void warp_minmax_bf16(uint4 w, float& mn, float& mx) {
+    const uint32_t mn2 = bmin2(bmin2(w.x, w.y), bmin2(w.z, w.w));
+    const uint32_t mx2 = bmax2(bmax2(w.x, w.y), bmax2(w.z, w.w));
+    const uint32_t nmx2 = mx2 ^ 0x80008000u;  // -max, exact
+    uint32_t r = bmin2(__byte_perm(mn2, nmx2, 0x5410), __byte_perm(mn2, nmx2, 0x7632));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) r = bmin2(r, __shfl_xor_sync(0xffffffffu, r, o));
+    mn = __uint_as_float(r << 16);
+    mx = __uint_as_float((r & 0xFFFF0000u) ^ 0x80000000u);
+}
+
 __device__ __forceinline__ float warp_min(float v) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));

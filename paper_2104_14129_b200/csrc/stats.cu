@@ -51,17 +51,6 @@ __device__ __forceinline__ uint4 ldg_nc_u4(const uint16_t* p) {
 }
 __device__ __forceinline__ uint4 ldg_nc_u4(const float*) { return make_uint4(0, 0, 0, 0); }
 
-// per-half min / max of two bf16x2 words
-__device__ __forceinline__ uint32_t bmin2(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
-__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
 
 template <typename T, bool kFast>
 __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) {
@@ -90,15 +79,11 @@ __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) 
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 if (gw + u < gcount) {
-                    const uint32_t mn2 = bmin2(bmin2(q[u].x, q[u].y), bmin2(q[u].z, q[u].w));
-                    const uint32_t mx2 = bmax2(bmax2(q[u].x, q[u].y), bmax2(q[u].z, q[u].w));
-                    const uint32_t nmx2 = mx2 ^ 0x80008000u;  // -max, exact
-                    uint32_t r = bmin2(__byte_perm(mn2, nmx2, 0x5410), __byte_perm(mn2, nmx2, 0x7632));
-#pragma unroll
-                    for (int o = 16; o >= 1; o >>= 1) r = bmin2(r, __shfl_xor_sync(kFull, r, o));
+                    float mn, mx;
+                    warp_minmax_bf16(q[u], mn, mx);
                     if (lane == u) {
-                        myMn = __uint_as_float(r << 16);
-                        myMx = __uint_as_float((r & 0xFFFF0000u) ^ 0x80000000u);
+                        myMn = mn;
+                        myMx = mx;
                     }
                 }
             }
