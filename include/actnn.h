@@ -219,7 +219,9 @@ size_t actnn_allocate_layers_ws_bytes(int64_t L, int64_t N, uint32_t level_mask)
  *   sens [L*N] fp64 (layer-major; actnn_group_stats outputs of every layer),
  *   gscale [L*N] fp64 or NULL (gradient estimates), lconst [L] fp64 or NULL
  *   (per-layer constants), all finite and >= 0;
- *   D_host [L] HOST array of per-sample feature dimensions D_l (1 <= D_l <= 2^24);
+ *   D_host [L] HOST array of per-sample feature dimensions D_l (1 <= D_l <= 2^24),
+ *   read at call time (it travels in the launch parameters; the caller may
+ *   reuse it as soon as the call returns);
  *   L in 0..ACTNN_MAX_LAYERS (else ACTNN_ERR_UNSUPPORTED), L*N*(levels-1) <= 2^31;
  *   b_total: total bits; ACTNN_ERR_BUDGET when below sum_l D_l N min-width;
  *   bits [L*N] u8 output; budgets [L] i64 output: b^(l) = sum_n b_ln, the
