@@ -45,10 +45,10 @@ constexpr unsigned kFull = 0xffffffffu;
 template <typename T>
 struct Cfg;
 #ifndef ACTNN_Q_S32
-#define ACTNN_Q_S32 3
+#define ACTNN_Q_S32 2
 #endif
 #ifndef ACTNN_Q_MINB32
-#define ACTNN_Q_MINB32 2
+#define ACTNN_Q_MINB32 3
 #endif
 #ifndef ACTNN_Q_S16
 #define ACTNN_Q_S16 4
