@@ -535,6 +535,9 @@ def main():
     adapt = None
     if plan.mixed and world == 1 and not args.no_adapt:
         adapt = run_adapt(A, plan, xs, wl, s_in, torch, peak, barrier)
+    contexts = None
+    if world == 1 and not args.no_adapt:
+        contexts = run_contexts(A, xs, wl, torch, peak, barrier)
     # ---- e2e through the public API with host buffers (per-layer pipeline)
     e2e = None
     if not args.no_e2e:
@@ -562,6 +565,8 @@ def main():
         line["e2e"] = e2e
     if adapt is not None:
         line["adapt"] = adapt
+    if contexts is not None:
+        line["contexts"] = contexts
     if rank == 0 and world == 1 and not args.no_cpu:
         cb, _ = cpu_sample(wl, wl.acts, args, args.cpu_seconds, W.quant_seed, torch)
         line["cpu_baseline"] = cb
@@ -570,6 +575,49 @@ def main():
     if dist_on:
         dist.destroy_process_group()
     return 0
+
+
+def run_contexts(A, xs, wl, torch, peak, barrier, reps=5):
+    """NEXT-4 side measurement: the lossless contexts of a Conv-BN-ReLU-MaxPool
+    block on the largest tensor of the set (ResNet stem, 64 x 112 x 112 per
+    sample): ReLU 1-bit mask pack (+ y) and its backward, 3x3/2 max pool with
+    the 8-bit argmax and its backward.  Algorithmic bytes per call / event time."""
+    x = max(xs, key=lambda t: t.numel())
+    N = x.shape[0]
+    C, H, W = 64, 112, 112
+    if x.numel() != N * C * H * W:
+        return None
+    x4 = x.view(N, C, H, W)
+    s = x.element_size()
+    E = x.numel()
+    cs = torch.cuda.current_stream()
+
+    def t(fn):
+        fn()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        for _ in range(reps):
+            fn()
+        b.record(cs)
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    mask, y = A.relu_pack(x, want_y=True)
+    t_pack = t(lambda: A.relu_pack(x, want_y=True))
+    t_rb = t(lambda: A.relu_backward(mask, x))
+    yp, idx = A.maxpool2d(x4, 3, 2, 1)
+    t_pf = t(lambda: A.maxpool2d(x4, 3, 2, 1))
+    t_pb = t(lambda: A.maxpool2d_backward(idx, yp, H, W, 3, 2, 1))
+    EO = yp.numel()
+    rows = {"relu_pack": (t_pack, E * s + E // 8 + E * s),
+            "relu_backward": (t_rb, E // 8 + 2 * E * s),
+            "maxpool2d_forward": (t_pf, E * s + EO * (s + 1)),
+            "maxpool2d_backward": (t_pb, EO * (s + 1) + E * s)}
+    return {k: {"ms": ms, "GBps": by / (ms * 1e-3) / 1e9, "frac": by / (ms * 1e-3) / 1e9 / peak,
+                "algorithmic_bytes": by} for k, (ms, by) in rows.items()} | {
+        "tensor": f"{N}x{C}x{H}x{W} {wl.dtype}", "note": "NEXT-4 (P:1388-1419) side measurement, "
+        "not part of the step"}
 
 
 def run_adapt(A, plan, xs, wl, s_in, torch, peak, barrier, reps=5):

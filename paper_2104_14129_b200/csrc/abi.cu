@@ -537,6 +537,9 @@ static actnn_status_t pool_args(const char* fn, actnn_dtype_t dt, int64_t NC, in
     if (kh * kw > 256)
         return fail(ACTNN_ERR_UNSUPPORTED, "%s: %d taps do not fit the 8-bit index", fn,
                     kh * kw);
+    if (H * W >= (1ll << 31) || (int64_t)kh * dh + H + ph >= (1ll << 30) ||
+        (int64_t)kw * dw + W + pw >= (1ll << 30))
+        return fail(ACTNN_ERR_UNSUPPORTED, "%s: planes of 2^31 or more positions", fn);
     a->dt = (int)dt;
     a->NC = NC;
     a->H = H;

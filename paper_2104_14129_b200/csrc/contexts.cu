@@ -15,6 +15,8 @@
 // (row-major a * kw + b).  Backward: thread per input element, a gather over
 // the windows that contain it in increasing output order (no atomics, so the
 // fp32 sum order is fixed and equals the oracle's / PyTorch CPU's).
+#include <algorithm>
+
 #include "device.cuh"
 #include "launch.h"
 
@@ -185,37 +187,45 @@ struct Pool {
     int kh, kw, sh, sw, ph, pw, dh, dw;
 };
 
+// One launch covers planes p = blockIdx.y, blockIdx.y + gridDim.y, ... and, in
+// each plane, output positions blockIdx.x * kBlock + threadIdx.x + k * span:
+// all index arithmetic is 32-bit (a plane has < 2^31 positions) and the window
+// taps are read through L1 (each input is read by ~kh kw / (sh sw) windows).
+// kS2: stride 2 in both dimensions (every ResNet max pool) -> shifts.
 template <typename T>
 __global__ void __launch_bounds__(kBlock) maxpool_fwd_kernel(const T* __restrict__ x, Pool g,
                                                              T* __restrict__ y,
                                                              uint8_t* __restrict__ idx) {
-    const int64_t total = g.NC * g.OH * g.OW;
-    for (int64_t o = (int64_t)blockIdx.x * kBlock + threadIdx.x; o < total;
-         o += (int64_t)gridDim.x * kBlock) {
-        const int64_t j = o % g.OW;
-        const int64_t t = o / g.OW;
-        const int64_t i = t % g.OH;
-        const int64_t p = t / g.OH;
-        const T* plane = x + p * g.H * g.W;
-        float best = 0.0f;
-        T bestv = (T)0;
-        int arg = -1;
-        for (int a = 0; a < g.kh; ++a) {
-            const int64_t r = i * g.sh - g.ph + (int64_t)a * g.dh;
-            if (r < 0 || r >= g.H) continue;
-            for (int b = 0; b < g.kw; ++b) {
-                const int64_t c = j * g.sw - g.pw + (int64_t)b * g.dw;
-                if (c < 0 || c >= g.W) continue;
-                const float v = widen1(plane, r * g.W + c);
-                if (arg < 0 || v > best) {  // first maximum in row-major tap order
-                    best = v;
-                    bestv = plane[r * g.W + c];
-                    arg = a * g.kw + b;
+    const int H = (int)g.H, W = (int)g.W, OW = (int)g.OW;
+    const int P = (int)(g.OH * g.OW);
+    const int span = gridDim.x * kBlock;
+    for (int64_t p = blockIdx.y; p < g.NC; p += gridDim.y) {
+        const T* __restrict__ plane = x + p * g.H * g.W;
+        for (int o = blockIdx.x * kBlock + threadIdx.x; o < P; o += span) {
+            const int i = o / OW;
+            const int j = o - i * OW;
+            float best = 0.0f;
+            T bestv = (T)0;
+            int arg = -1;
+            const int r0 = i * g.sh - g.ph, c0 = j * g.sw - g.pw;
+            for (int a = 0; a < g.kh; ++a) {
+                const int r = r0 + a * g.dh;
+                if (r < 0 || r >= H) continue;
+                for (int b = 0; b < g.kw; ++b) {
+                    const int c = c0 + b * g.dw;
+                    if (c < 0 || c >= W) continue;
+                    const T raw = __ldg(plane + r * W + c);
+                    const float v = widen1(&raw, 0);
+                    if (arg < 0 || v > best) {  // first maximum in row-major tap order
+                        best = v;
+                        bestv = raw;
+                        arg = a * g.kw + b;
+                    }
                 }
             }
+            y[p * P + o] = bestv;
+            idx[p * P + o] = (uint8_t)arg;
         }
-        y[o] = bestv;
-        idx[o] = (uint8_t)arg;
     }
 }
 
@@ -225,35 +235,150 @@ __device__ __forceinline__ void store_acc(uint16_t* p, float v) {
 }
 
 // grad_x gather: windows containing (r, c) in increasing (oh, ow) order; tap
-// a gives oh = (r + ph - a dh) / sh, so a runs downwards for ascending oh.
-template <typename T>
+// a gives oh = (r + ph - a dh) / sh, so a runs downwards for ascending oh
+// (the oracle's accumulation order, bit for bit).
+template <typename T, bool kS2>
 __global__ void __launch_bounds__(kBlock) maxpool_bwd_kernel(const uint8_t* __restrict__ idx,
                                                              const T* __restrict__ gy, Pool g,
                                                              T* __restrict__ gx) {
-    const int64_t total = g.NC * g.H * g.W;
-    for (int64_t q = (int64_t)blockIdx.x * kBlock + threadIdx.x; q < total;
-         q += (int64_t)gridDim.x * kBlock) {
-        const int64_t c = q % g.W;
-        const int64_t t = q / g.W;
-        const int64_t r = t % g.H;
-        const int64_t p = t / g.H;
-        const int64_t obase = p * g.OH * g.OW;
-        float acc = 0.0f;
-        for (int a = g.kh - 1; a >= 0; --a) {
-            const int64_t u = r + g.ph - (int64_t)a * g.dh;
-            if (u < 0 || u % g.sh) continue;
-            const int64_t oh = u / g.sh;
-            if (oh >= g.OH) continue;
-            for (int b = g.kw - 1; b >= 0; --b) {
-                const int64_t v = c + g.pw - (int64_t)b * g.dw;
-                if (v < 0 || v % g.sw) continue;
-                const int64_t ow = v / g.sw;
-                if (ow >= g.OW) continue;
-                const int64_t o = obase + oh * g.OW + ow;
-                if ((int)__ldg(idx + o) == a * g.kw + b) acc += widen1(gy, o);
+    const int W = (int)g.W, OH = (int)g.OH, OW = (int)g.OW;
+    const int P = (int)(g.H * g.W), OP = OH * OW;
+    const int span = gridDim.x * kBlock;
+    for (int64_t p = blockIdx.y; p < g.NC; p += gridDim.y) {
+        const uint8_t* __restrict__ ip = idx + p * OP;
+        const T* __restrict__ gp = gy + p * OP;
+        for (int q = blockIdx.x * kBlock + threadIdx.x; q < P; q += span) {
+            const int r = q / W;
+            const int c = q - r * W;
+            float acc = 0.0f;
+            for (int a = g.kh - 1; a >= 0; --a) {
+                const int u = r + g.ph - a * g.dh;
+                if (u < 0) continue;
+                int oh;
+                if (kS2) {
+                    if (u & 1) continue;
+                    oh = u >> 1;
+                } else {
+                    if (u % g.sh) continue;
+                    oh = u / g.sh;
+                }
+                if (oh >= OH) continue;
+                for (int b = g.kw - 1; b >= 0; --b) {
+                    const int v = c + g.pw - b * g.dw;
+                    if (v < 0) continue;
+                    int ow;
+                    if (kS2) {
+                        if (v & 1) continue;
+                        ow = v >> 1;
+                    } else {
+                        if (v % g.sw) continue;
+                        ow = v / g.sw;
+                    }
+                    if (ow >= OW) continue;
+                    const int o = oh * OW + ow;
+                    if ((int)__ldg(ip + o) == a * g.kw + b) acc += widen1(gp, o);
+                }
+            }
+            store_acc(gx + p * P + q, acc);
+        }
+    }
+}
+
+// The ResNet max pool (3x3, stride 2, padding 1, dilation 1), specialised.
+// Forward: the window's taps unrolled with compile-time offsets.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) maxpool_fwd_k3s2_kernel(const T* __restrict__ x, Pool g,
+                                                                  T* __restrict__ y,
+                                                                  uint8_t* __restrict__ idx) {
+    const int H = (int)g.H, W = (int)g.W, OW = (int)g.OW;
+    const int P = (int)(g.OH * g.OW);
+    const int span = gridDim.x * kBlock;
+    for (int64_t p = blockIdx.y; p < g.NC; p += gridDim.y) {
+        const T* __restrict__ plane = x + p * g.H * g.W;
+        for (int o = blockIdx.x * kBlock + threadIdx.x; o < P; o += span) {
+            const int i = o / OW;
+            const int j = o - i * OW;
+            float best = 0.0f;
+            T bestv = (T)0;
+            int arg = -1;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int r = 2 * i - 1 + a;
+                if (r < 0 || r >= H) continue;
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    const int c = 2 * j - 1 + b;
+                    if (c < 0 || c >= W) continue;
+                    const T raw = __ldg(plane + r * W + c);
+                    const float v = widen1(&raw, 0);
+                    if (arg < 0 || v > best) {
+                        best = v;
+                        bestv = raw;
+                        arg = a * 3 + b;
+                    }
+                }
+            }
+            y[p * P + o] = bestv;
+            idx[p * P + o] = (uint8_t)arg;
+        }
+    }
+}
+
+// Backward: one thread per 2x2 block of inputs (rows 2i, 2i+1; columns 2j,
+// 2j+1), which are covered only by the windows (i, j), (i, j+1), (i+1, j),
+// (i+1, j+1): input (2i+s, 2j+t) takes tap a = 1 + s (window row i) or a = 0
+// (row i + 1, s = 1), likewise b -- no divergence, four (idx, grad) reads per
+// four outputs, contributions added in increasing (oh, ow) order as the oracle.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_kernel(const uint8_t* __restrict__ idx,
+                                                                  const T* __restrict__ gy, Pool g,
+                                                                  T* __restrict__ gx) {
+    const int H = (int)g.H, W = (int)g.W, OH = (int)g.OH, OW = (int)g.OW;
+    const int BH = (H + 1) >> 1, BW = (W + 1) >> 1;  // 2x2 blocks per plane
+    const int PB = BH * BW, OP = OH * OW;
+    const int span = gridDim.x * kBlock;
+    for (int64_t p = blockIdx.y; p < g.NC; p += gridDim.y) {
+        const uint8_t* __restrict__ ip = idx + p * OP;
+        const T* __restrict__ gp = gy + p * OP;
+        T* __restrict__ out = gx + p * g.H * g.W;
+        for (int q = blockIdx.x * kBlock + threadIdx.x; q < PB; q += span) {
+            const int i = q / BW;
+            const int j = q - i * BW;
+            // the four windows (absent ones never match: tap 255)
+            int k00 = 255, k01 = 255, k10 = 255, k11 = 255;
+            float g00 = 0.0f, g01 = 0.0f, g10 = 0.0f, g11 = 0.0f;
+            if (i < OH && j < OW) { k00 = __ldg(ip + i * OW + j); g00 = widen1(gp, i * OW + j); }
+            if (i < OH && j + 1 < OW) { k01 = __ldg(ip + i * OW + j + 1); g01 = widen1(gp, i * OW + j + 1); }
+            if (i + 1 < OH && j < OW) { k10 = __ldg(ip + (i + 1) * OW + j); g10 = widen1(gp, (i + 1) * OW + j); }
+            if (i + 1 < OH && j + 1 < OW) {
+                k11 = __ldg(ip + (i + 1) * OW + j + 1);
+                g11 = widen1(gp, (i + 1) * OW + j + 1);
+            }
+            const int r = 2 * i, c = 2 * j;
+            // (2i, 2j): window (i, j) tap (1, 1)
+            float a00 = 0.0f;
+            if (k00 == 4) a00 += g00;
+            // (2i, 2j+1): (i, j) tap (1, 2), then (i, j+1) tap (1, 0)
+            float a01 = 0.0f;
+            if (k00 == 5) a01 += g00;
+            if (k01 == 3) a01 += g01;
+            // (2i+1, 2j): (i, j) tap (2, 1), then (i+1, j) tap (0, 1)
+            float a10 = 0.0f;
+            if (k00 == 7) a10 += g00;
+            if (k10 == 1) a10 += g10;
+            // (2i+1, 2j+1): (i, j) (2, 2), (i, j+1) (2, 0), (i+1, j) (0, 2), (i+1, j+1) (0, 0)
+            float a11 = 0.0f;
+            if (k00 == 8) a11 += g00;
+            if (k01 == 6) a11 += g01;
+            if (k10 == 2) a11 += g10;
+            if (k11 == 0) a11 += g11;
+            store_acc(out + r * W + c, a00);
+            if (c + 1 < W) store_acc(out + r * W + c + 1, a01);
+            if (r + 1 < H) {
+                store_acc(out + (r + 1) * W + c, a10);
+                if (c + 1 < W) store_acc(out + (r + 1) * W + c + 1, a11);
             }
         }
-        store_acc(gx + q, acc);
     }
 }
 
@@ -310,16 +435,28 @@ cudaError_t relu_backward_t(const ReluArgs& a, cudaStream_t s) {
 template <typename T>
 cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
     Pool g{a.NC, a.H, a.W, a.OH, a.OW, a.kh, a.kw, a.sh, a.sw, a.ph, a.pw, a.dh, a.dw};
-    if (!backward) {
-        const int grid = grid_for((const void*)maxpool_fwd_kernel<T>, kBlock, 0,
-                                  (a.NC * a.OH * a.OW + kBlock - 1) / kBlock);
-        maxpool_fwd_kernel<T><<<grid, kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
-                                                      static_cast<T*>(a.out), a.idx);
+    const int64_t per_plane = backward ? a.H * a.W : a.OH * a.OW;
+    const int bx = (int)std::min<int64_t>((per_plane + kBlock - 1) / kBlock, 64);
+    const int by = (int)std::min<int64_t>(a.NC, 65535);
+    const bool k3s2 = a.kh == 3 && a.kw == 3 && a.sh == 2 && a.sw == 2 && a.ph == 1 &&
+                      a.pw == 1 && a.dh == 1 && a.dw == 1;
+    if (!backward && k3s2) {
+        maxpool_fwd_k3s2_kernel<T><<<dim3(bx, by), kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
+                                                                  static_cast<T*>(a.out), a.idx);
+    } else if (!backward) {
+        maxpool_fwd_kernel<T><<<dim3(bx, by), kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
+                                                             static_cast<T*>(a.out), a.idx);
+    } else if (k3s2) {
+        const int64_t blocks = ((a.H + 1) / 2) * ((a.W + 1) / 2);
+        const int bxb = (int)std::min<int64_t>((blocks + kBlock - 1) / kBlock, 64);
+        maxpool_bwd_k3s2_kernel<T><<<dim3(bxb, by), kBlock, 0, s>>>(
+            a.idx, static_cast<const T*>(a.in), g, static_cast<T*>(a.out));
+    } else if (a.sh == 2 && a.sw == 2) {
+        maxpool_bwd_kernel<T, true><<<dim3(bx, by), kBlock, 0, s>>>(
+            a.idx, static_cast<const T*>(a.in), g, static_cast<T*>(a.out));
     } else {
-        const int grid = grid_for((const void*)maxpool_bwd_kernel<T>, kBlock, 0,
-                                  (a.NC * a.H * a.W + kBlock - 1) / kBlock);
-        maxpool_bwd_kernel<T><<<grid, kBlock, 0, s>>>(a.idx, static_cast<const T*>(a.in), g,
-                                                      static_cast<T*>(a.out));
+        maxpool_bwd_kernel<T, false><<<dim3(bx, by), kBlock, 0, s>>>(
+            a.idx, static_cast<const T*>(a.in), g, static_cast<T*>(a.out));
     }
     return cudaGetLastError();
 }
