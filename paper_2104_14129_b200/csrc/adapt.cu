@@ -51,21 +51,32 @@ __global__ void __launch_bounds__(GCfg<T>::Block) grad_sqnorm_kernel(GParams p) 
     __shared__ double sQ[kChunk];
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
+    const int gw = w * kGU;
     const T* __restrict__ g = static_cast<const T*>(p.g);
     const int64_t tiles = p.N * p.nch;
+    // fast path: the next tile's words are in flight while this tile is reduced
+    uint4 cur[kGU][2], nxt[kGU][2];
+    auto load_tile = [&](int64_t t, uint4 (&q)[kGU][2]) {
+        const int64_t n = t / p.nch;
+        const int64_t g0 = (t - n * p.nch) * kChunk;
+        const int gcount = (int)min((int64_t)kChunk, p.ng - g0);
+        const T* src = g + n * p.D + (g0 + gw) * kG + lane * 8;
+#pragma unroll
+        for (int u = 0; u < kGU; ++u)
+            if (gw + u < gcount) ldg_raw8(src + u * kG, q[u]);
+    };
+    if (kFast && (int64_t)blockIdx.x < tiles) load_tile(blockIdx.x, cur);
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int64_t n = t / p.nch;
         const int64_t c = t - n * p.nch;
         const int64_t g0 = c * kChunk;
         const int gcount = (int)min((int64_t)kChunk, p.ng - g0);
-        const int gw = w * kGU;
         double myQ = 0.0;
         float v[kGU][8];
         if (kFast) {
-            const T* src = g + n * p.D + (g0 + gw) * kG + lane * 8;
+            if (t + gridDim.x < tiles) load_tile(t + gridDim.x, nxt);
 #pragma unroll
-            for (int u = 0; u < kGU; ++u)
-                if (gw + u < gcount) load8(src + u * kG, v[u]);
+            for (int u = 0; u < kGU; ++u) raw8_f32<T>(cur[u], v[u]);
         } else {
 #pragma unroll
             for (int u = 0; u < kGU; ++u) {
@@ -104,6 +115,13 @@ __global__ void __launch_bounds__(GCfg<T>::Block) grad_sqnorm_kernel(GParams p) 
             if (lane == 0) p.T[c * p.N + n] = q;
         }
         __syncthreads();
+        if (kFast) {
+#pragma unroll
+            for (int u = 0; u < kGU; ++u) {
+                cur[u][0] = nxt[u][0];
+                cur[u][1] = nxt[u][1];
+            }
+        }
     }
     __shared__ unsigned int s_last;
     __threadfence();

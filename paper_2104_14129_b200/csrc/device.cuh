@@ -177,6 +177,39 @@ __device__ __forceinline__ void load8(const uint16_t* p, float v[8]) {
     v[7] = __uint_as_float(d & 0xFFFF0000u);
 }
 
+// A lane's 8 elements of a group as raw words (no widening): fp32 one 256-bit
+// load into r[0..1], bf16 one 128-bit load into r[0].
+__device__ __forceinline__ void ldg_raw8(const float* p, uint4 (&r)[2]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0].x), "=r"(r[0].y), "=r"(r[0].z), "=r"(r[0].w), "=r"(r[1].x),
+                   "=r"(r[1].y), "=r"(r[1].z), "=r"(r[1].w)
+                 : "l"(p));
+}
+__device__ __forceinline__ void ldg_raw8(const uint16_t* p, uint4 (&r)[2]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0].x), "=r"(r[0].y), "=r"(r[0].z), "=r"(r[0].w)
+                 : "l"(p));
+}
+// ... and widened to fp32 (bf16 -> fp32 is exact)
+template <typename T>
+__device__ __forceinline__ void raw8_f32(const uint4 (&r)[2], float v[8]) {
+    if constexpr (sizeof(T) == 4) {
+        v[0] = __uint_as_float(r[0].x); v[1] = __uint_as_float(r[0].y);
+        v[2] = __uint_as_float(r[0].z); v[3] = __uint_as_float(r[0].w);
+        v[4] = __uint_as_float(r[1].x); v[5] = __uint_as_float(r[1].y);
+        v[6] = __uint_as_float(r[1].z); v[7] = __uint_as_float(r[1].w);
+    } else {
+        v[0] = __uint_as_float(__byte_perm(r[0].x, 0u, 0x1044));
+        v[1] = __uint_as_float(r[0].x & 0xFFFF0000u);
+        v[2] = __uint_as_float(__byte_perm(r[0].y, 0u, 0x1044));
+        v[3] = __uint_as_float(r[0].y & 0xFFFF0000u);
+        v[4] = __uint_as_float(__byte_perm(r[0].z, 0u, 0x1044));
+        v[5] = __uint_as_float(r[0].z & 0xFFFF0000u);
+        v[6] = __uint_as_float(__byte_perm(r[0].w, 0u, 0x1044));
+        v[7] = __uint_as_float(r[0].w & 0xFFFF0000u);
+    }
+}
+
 __device__ __forceinline__ float load1(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float load1(const uint16_t* p) {
     return __uint_as_float((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p)) << 16);
