@@ -152,17 +152,12 @@ __device__ __forceinline__ void quant_group(const float v[8], float Z, float inv
 #else
     const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
 #endif
+    // every lane stores its own b bytes; one warp store fills the group's
+    // 32 b-byte segment (measured faster than shuffling into word stores)
     if constexpr (b == 2) {
-        const uint32_t pl = codes_small<2>(v, Z, inv14, o);
-        const uint32_t q = __shfl_down_sync(kFull, pl, 1);
-        if (!(lane & 1)) *reinterpret_cast<uint32_t*>(seg + lane * 2) = pl | (q << 16);
+        reinterpret_cast<uint16_t*>(seg)[lane] = (uint16_t)codes_small<2>(v, Z, inv14, o);
     } else if constexpr (b == 1) {
-        const uint32_t pl = codes_small<1>(v, Z, inv14, o);
-        const uint32_t q1 = __shfl_down_sync(kFull, pl, 1);
-        const uint32_t q2 = __shfl_down_sync(kFull, pl, 2);
-        const uint32_t q3 = __shfl_down_sync(kFull, pl, 3);
-        if (!(lane & 3))
-            *reinterpret_cast<uint32_t*>(seg + lane) = pl | (q1 << 8) | (q2 << 16) | (q3 << 24);
+        seg[lane] = (uint8_t)codes_small<1>(v, Z, inv14, o);
     } else {
         uint32_t code[8];
         codes_wide(v, Z, inv14, o, code);

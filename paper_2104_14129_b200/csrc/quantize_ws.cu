@@ -52,6 +52,9 @@ namespace {
 #ifndef ACTNN_WS_CWAIT
 #define ACTNN_WS_CWAIT mbar_wait
 #endif
+#ifndef ACTNN_WS_NARROW_ST
+#define ACTNN_WS_NARROW_ST 1
+#endif
 #ifndef ACTNN_WS_PROD
 #define ACTNN_WS_PROD 2
 #endif
@@ -128,6 +131,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 template <int b>
 __device__ __forceinline__ void ws_store(const float v[8], float Z, float inv14,
                                          const Philox4& o, uint8_t* seg, int lane) {
+#if ACTNN_WS_NARROW_ST
+    // every lane stores its own b bytes: one warp store fills the group's
+    // 32 b-byte segment (whole sectors), no shuffles
+    if constexpr (b == 2) {
+        reinterpret_cast<uint16_t*>(seg)[lane] = (uint16_t)codes_small<2>(v, Z, inv14, o);
+    } else if constexpr (b == 1) {
+        seg[lane] = (uint8_t)codes_small<1>(v, Z, inv14, o);
+    } else {
+#else
     if constexpr (b == 2) {
         const uint32_t pl = codes_small<2>(v, Z, inv14, o);
         const uint32_t q = __shfl_down_sync(kFull, pl, 1);
@@ -140,6 +152,7 @@ __device__ __forceinline__ void ws_store(const float v[8], float Z, float inv14,
         if (!(lane & 3))
             *reinterpret_cast<uint32_t*>(seg + lane) = pl | (q1 << 8) | (q2 << 16) | (q3 << 24);
     } else {
+#endif
         const uint32_t w[4] = {o.x, o.y, o.z, o.w};
         uint32_t code[8];
 #pragma unroll
