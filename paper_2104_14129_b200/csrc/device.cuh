@@ -100,6 +100,36 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, const
     return Philox4{c0, c1, c2, c3};
 }
 
+// Philox4x32-10 for a counter whose high word is 0 (every tensor below 2^35
+// elements, checked by the launchers): round 0 leaves c0 = k0 for every lane,
+// so round 1's first product M0 * k0 is the same for all threads -- ptxas
+// computes it once in the uniform datapath -- and each call costs 18 instead of
+// 19 per-thread IMAD.WIDE.  Same outputs as philox4x32_10(c0, 0, rk).
+__device__ __forceinline__ Philox4 philox4x32_10_c32(uint32_t c0, const RoundKeys& rk) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mulwide(c0, 0xD2511F53u, hi0, lo0);  // round 0 (c1 = c2 = c3 = 0)
+    const uint32_t x2 = hi0 ^ rk.k[1], x3 = lo0;
+    uint32_t ahi, alo;
+    mulwide(rk.k[0], 0xD2511F53u, ahi, alo);  // round 1, first product: uniform
+    mulwide(x2, 0xCD9E8D57u, hi1, lo1);
+    uint32_t a0 = hi1 ^ rk.k[2];
+    uint32_t a1 = lo1;
+    uint32_t a2 = ahi ^ x3 ^ rk.k[3];
+    uint32_t a3 = alo;
+#pragma unroll
+    for (int r = 2; r < 10; ++r) {
+        mulwide(a0, 0xD2511F53u, hi0, lo0);
+        mulwide(a2, 0xCD9E8D57u, hi1, lo1);
+        const uint32_t n0 = hi1 ^ a1 ^ rk.k[2 * r];
+        const uint32_t n2 = hi0 ^ a3 ^ rk.k[2 * r + 1];
+        a0 = n0;
+        a1 = lo1;
+        a2 = n2;
+        a3 = lo0;
+    }
+    return Philox4{a0, a1, a2, a3};
+}
+
 // 14-bit draw of element j (0..7) of an 8-element Philox block: 16-bit lane j.
 __device__ __forceinline__ uint32_t rnd14(const Philox4& o, int j) {
     const uint32_t w = (j >> 1) == 0 ? o.x : (j >> 1) == 1 ? o.y : (j >> 1) == 2 ? o.z : o.w;

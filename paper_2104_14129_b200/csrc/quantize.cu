@@ -150,7 +150,7 @@ __device__ __forceinline__ void quant_group(const float v[8], float Z, float inv
 #if ACTNN_Q_KEYS == 1
     const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk.k[0], rk.k[1]);
 #else
-    const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+    const Philox4 o = philox4x32_10_c32((uint32_t)blk, rk);
 #endif
     // every lane stores its own b bytes; one warp store fills the group's
     // 32 b-byte segment (measured faster than shuffling into word stores)
@@ -424,8 +424,12 @@ template <typename T, bool kStats>
 cudaError_t run(const QuantArgs& a, cudaStream_t s) {
     const int64_t nb = (a.ng + kU - 1) / kU;
     // fast path: 32-bit unit walk (N * ng, D, sample_base + N < 2^31)
+    // fast kernels: 32-bit unit walks, and Philox counters (global element
+    // index >> 3) below 2^32 (philox4x32_10_c32); larger problems take the
+    // generic kernel, which carries the full 64-bit counter
     const bool fits = a.N * a.ng < (1ll << 31) && a.D < (1ll << 31) &&
-                      a.sample_base + a.N < (1ll << 31);
+                      a.sample_base + a.N < (1ll << 31) &&
+                      (a.sample_base + a.N) * a.D <= (1ll << 35);
     if (a.fast && fits) {
         QParams p;
         p.x = a.x;
@@ -488,8 +492,12 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
 
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
     const bool stats = (a.gmin == nullptr);
+    // fast kernels: 32-bit unit walks, and Philox counters (global element
+    // index >> 3) below 2^32 (philox4x32_10_c32); larger problems take the
+    // generic kernel, which carries the full 64-bit counter
     const bool fits = a.N * a.ng < (1ll << 31) && a.D < (1ll << 31) &&
-                      a.sample_base + a.N < (1ll << 31);
+                      a.sample_base + a.N < (1ll << 31) &&
+                      (a.sample_base + a.N) * a.D <= (1ll << 35);
     // mixed path (group stats given): the warp-specialised kernel (quantize_ws.cu)
     if (!stats && a.fast && fits && !std::getenv("ACTNN_NO_WS")) return launch_quantize_ws(a, s);
     if (a.dt == 0) return stats ? run<float, true>(a, s) : run<float, false>(a, s);

@@ -223,7 +223,7 @@ __device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
             const uint64_t c = blk + (uint64_t)((h + q) * 32);
-            o[q] = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), rk);
+            o[q] = philox4x32_10_c32((uint32_t)c, rk);
         }
 #pragma unroll
         for (int q = 0; q < PH; ++q)
@@ -265,7 +265,7 @@ __device__ __forceinline__ void ws_unit_lazy(const T* st, const Desc& d, uint8_t
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
             const uint64_t blk = blk0 + (uint64_t)((h + q) * 32 + lane);
-            o[q] = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+            o[q] = philox4x32_10_c32((uint32_t)blk, rk);
         }
 #pragma unroll
         for (int q = 0; q < PH; ++q)
@@ -285,7 +285,7 @@ __device__ __forceinline__ void ws_full_unit(const float (&v)[U][8], const float
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
             const uint64_t c = blk + (uint64_t)((h + q) * 32);
-            o[q] = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), rk);
+            o[q] = philox4x32_10_c32((uint32_t)c, rk);
         }
 #pragma unroll
         for (int q = 0; q < PH; ++q)
@@ -334,7 +334,7 @@ __device__ __forceinline__ void ws_unit_eager(const T* st, const Desc& d, uint8_
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
             const uint64_t blk = blk0 + (uint64_t)((h + q) * 32 + lane);
-            o[q] = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+            o[q] = philox4x32_10_c32((uint32_t)blk, rk);
         }
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
@@ -381,7 +381,7 @@ __device__ __forceinline__ void ws_packed_full(const uint4 (&raw)[8], const floa
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
             const uint64_t c = blk + (uint64_t)((h + q) * 32);
-            o[q] = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), rk);
+            o[q] = philox4x32_10_c32((uint32_t)c, rk);
         }
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
@@ -426,7 +426,7 @@ __device__ __forceinline__ void ws_unit_packed(const uint16_t* st, const Desc& d
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
             const uint64_t blk = blk0 + (uint64_t)((h + q) * 32 + lane);
-            o[q] = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk);
+            o[q] = philox4x32_10_c32((uint32_t)blk, rk);
         }
 #pragma unroll
         for (int q = 0; q < PH; ++q) {

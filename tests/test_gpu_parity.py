@@ -407,3 +407,18 @@ def test_pipelined_step_graph_with_nccl_gather(A, W):
                                                      "graph_nccl_check.py")],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("sample_base", [524284, 524285, 2 ** 30])
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_philox_counter_high_word(A, sample_base, two_pass):
+    """Global element indices up to exactly 2^35 (524284: the last Philox
+    counter is 2^32 - 1, fast kernels with the 32-bit-counter Philox) and past
+    it (counter high word non-zero: the generic kernel carries the 64-bit
+    counter); both equal the oracle."""
+    D = 65536
+    g = torch.Generator(device=DEV).manual_seed(sample_base)
+    x = torch.randn((4, D), generator=g, device=DEV)
+    for bits in ([1, 2, 4, 8], [2, 2, 2, 2]):
+        p, ref = run_both(A, x, bits, seed=77, sample_base=sample_base, two_pass=two_pass)
+        assert_packed_equal(p, ref, 4)
