@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
 
     uint32_t pn = gw / p.nb, pj = gw % p.nb;
     uint32_t n = pn, j = pj;
+#ifndef ACTNN_DQ_STOREONLY
     if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < kS; ++s) {
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
             advance(pn, pj);
         }
     }
+#endif
     int stage = 0;
     uint32_t phase = 0;
     while (n < p.N) {
@@ -210,6 +212,14 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
         TO* dst = out + (uint64_t)n * p.D + (uint64_t)j * (kU * kG);
         const uint8_t* st = ring + stage * kStage;
         const uint32_t g = n * p.ng + j * kU;
+#ifdef ACTNN_DQ_STOREONLY  // diagnostics: K4's store pattern alone (no reads, no codes)
+        if (true) {
+            const float o8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int u = 0; u < gcount_of(j); ++u) store8(reinterpret_cast<float*>(dst) + u * kG + lane * 8, o8);
+            advance(n, j);
+            continue;
+        }
+#endif
         mbar_wait(&bars[stage], phase);
         float zq[kU], sq[kU];
         if constexpr (kB16) {
@@ -223,12 +233,19 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
                 sq[u] = __shfl_sync(0xffffffffu, sl, u);
             }
         } else {
-            const float* zp = kMeta ? reinterpret_cast<const float*>(st + kPay) : p.zmin + g;
-            const float* sp = kMeta ? reinterpret_cast<const float*>(st + kPay + 4 * kU) : p.scale + g;
+            if (kMeta && kU == 4) {  // the unit's 4 zero points / scales: two 16-byte loads
+                const float4 z4 = *reinterpret_cast<const float4*>(st + kPay);
+                const float4 s4 = *reinterpret_cast<const float4*>(st + kPay + 16);
+                zq[0] = z4.x; zq[1] = z4.y; zq[2] = z4.z; zq[3] = z4.w;
+                sq[0] = s4.x; sq[1] = s4.y; sq[2] = s4.z; sq[3] = s4.w;
+            } else {
+                const float* zp = kMeta ? reinterpret_cast<const float*>(st + kPay) : p.zmin + g;
+                const float* sp = kMeta ? reinterpret_cast<const float*>(st + kPay + 4 * kU) : p.scale + g;
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                zq[u] = u < gcount ? zp[u] : 0.0f;
-                sq[u] = u < gcount ? sp[u] : 0.0f;
+                for (int u = 0; u < kU; ++u) {
+                    zq[u] = u < gcount ? zp[u] : 0.0f;
+                    sq[u] = u < gcount ? sp[u] : 0.0f;
+                }
             }
         }
         if (b == 2) dequant_unit_any<TO, 2>(st, gcount, zq, sq, dst, lane);

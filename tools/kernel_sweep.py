@@ -28,6 +28,7 @@ for li in layers:
         ts = []
         for _ in range(reps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(2_000_000)  # ~1 ms: the launch is queued before the GPU reaches it
             a.record()
             fn()
             b.record()
