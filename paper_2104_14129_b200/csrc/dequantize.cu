@@ -221,6 +221,23 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
         }
 #endif
         mbar_wait(&bars[stage], phase);
+#ifdef ACTNN_DQ_NOCOMPUTE  // diagnostics: the TMA ring + stores, no unpack/dequantise
+        if (true) {
+            const float o8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int u = 0; u < gcount; ++u) store8(reinterpret_cast<float*>(dst) + u * kG + lane * 8, o8);
+            __syncwarp();
+            if (lane == 0) {
+                if (pn < p.N) issue(pn, pj, stage);
+                advance(pn, pj);
+            }
+            if (++stage == kS) {
+                stage = 0;
+                phase ^= 1u;
+            }
+            advance(n, j);
+            continue;
+        }
+#endif
         float zq[kU], sq[kU];
         if constexpr (kB16) {
             const uint32_t* wq = kMeta ? reinterpret_cast<const uint32_t*>(st + kPay) : p.meta + g;
