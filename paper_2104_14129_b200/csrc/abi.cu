@@ -426,10 +426,8 @@ actnn_status_t actnn_gradmag_scatter(double* table, int64_t T, const int64_t* id
 }
 
 size_t actnn_allocate_layers_ws_bytes(int64_t L, int64_t N, uint32_t level_mask) {
-    int Lv[8], m = 0;
     if (L < 0 || N < 0 || level_mask == 0 || (level_mask & ~0x1FEu)) return 0;
-    for (int b = 8; b >= 1; --b)
-        if (level_mask & (1u << b)) Lv[m++] = b;
+    const int m = __builtin_popcount(level_mask);  // number of allowed widths
     return allocate_layers_ws_bytes(L, N, m - 1);
 }
 

@@ -24,7 +24,6 @@ namespace actnn {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr unsigned kFullMask = 0xffffffffu;
 
 template <typename T>
 struct RV;  // elements per 256-bit access

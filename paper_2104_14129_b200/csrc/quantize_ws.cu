@@ -467,7 +467,6 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
     }
     fence_mbar_init();
     __syncthreads();
-    const uint32_t nwarps = gridDim.x * kCons;
 
     if (w >= kCons) {
         // ------------------------------------------------------------ producer

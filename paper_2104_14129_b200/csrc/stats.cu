@@ -49,7 +49,6 @@ __device__ __forceinline__ uint4 ldg_nc_u4(const uint16_t* p) {
                  : "l"(p));
     return r;
 }
-__device__ __forceinline__ uint4 ldg_nc_u4(const float*) { return make_uint4(0, 0, 0, 0); }
 
 
 template <typename T, bool kFast>
