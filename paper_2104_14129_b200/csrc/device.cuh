@@ -443,6 +443,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// S_n = ((0 + T[0][n]) + T[1][n]) + ... in chunk order (the O11 order), with
+// 16 chunk partials in flight per step: the last-CTA tail of K1 / K6 is a
+// dependent chain of L2 loads otherwise (98 chunks on the 822 MB tensors).
+__device__ __forceinline__ double sum_chunks_in_order(const double* T, int64_t nch, int64_t N,
+                                                      int64_t n) {
+    double s = 0.0;
+    int64_t c = 0;
+    for (; c + 16 <= nch; c += 16) {
+        double t[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) t[i] = __ldcg(T + (c + i) * N + n);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s = __dadd_rn(s, t[i]);
+    }
+    for (; c < nch; ++c) s = __dadd_rn(s, __ldcg(T + c * N + n));
+    return s;
+}
+
 // 8 fp32 (two 16-byte shared loads) / 8 bf16 (one) of a lane from a stage.
 __device__ __forceinline__ void lds8(const float* p, float v[8]) {
     const float4 a = reinterpret_cast<const float4*>(p)[0];

@@ -162,8 +162,7 @@ __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) 
     if (s_last) {
         __threadfence();
         for (int64_t n = threadIdx.x; n < p.N; n += kBlock) {
-            double s = 0.0;
-            for (int64_t c = 0; c < p.nch; ++c) s = __dadd_rn(s, __ldcg(p.T + c * p.N + n));
+            const double s = sum_chunks_in_order(p.T, p.nch, p.N, n);
             p.sens[n] = s;
         }
     }
