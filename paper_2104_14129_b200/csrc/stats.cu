@@ -20,6 +20,9 @@ namespace {
 
 // groups per warp per chunk: 4 (fp32: 4 KB in flight per warp) or 8 (bf16:
 // also 4 KB); a CTA has 32 / U warps so that a chunk is 32 groups.
+#ifndef ACTNN_K1_PREFETCH
+#define ACTNN_K1_PREFETCH 0  // 1: next tile in flight; measured slower (74 registers, 3 CTAs/SM)
+#endif
 #ifndef ACTNN_K1_U16
 #define ACTNN_K1_U16 4
 #endif
@@ -60,26 +63,39 @@ __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) 
     const int w = threadIdx.x >> 5;
     const T* __restrict__ x = static_cast<const T*>(p.x);
     const int64_t tiles = p.N * p.nch;
+    const int gw = w * kU;  // this warp's first group within a chunk
+    // fast path: the warp's words of the CTA's next tile are loaded before this
+    // tile is reduced (ACTNN_K1_PREFETCH), hiding one load latency per tile
+    uint4 cur[kU][2], nxt[kU][2];
+    auto load_tile = [&](int64_t t, uint4 (&q)[kU][2]) {
+        const int64_t n = t / p.nch;
+        const int64_t g0 = (t - n * p.nch) * kChunk;
+        const int gcount = (int)min((int64_t)kChunk, p.ng - g0);
+        const T* src = x + n * p.D + (g0 + gw) * kG + lane * 8;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (gw + u < gcount) ldg_raw8(src + u * kG, q[u]);
+    };
+    if (kFast && ACTNN_K1_PREFETCH && (int64_t)blockIdx.x < tiles) load_tile(blockIdx.x, cur);
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int64_t n = t / p.nch;
         const int64_t c = t - n * p.nch;
         const int64_t g0 = c * kChunk;
         const int gcount = (int)min((int64_t)kChunk, p.ng - g0);
-        const int gw = w * kU;  // this warp's first group within the chunk
         float myMn = 0.0f, myMx = 0.0f;
+        if (kFast && ACTNN_K1_PREFETCH) {
+            if (t + gridDim.x < tiles) load_tile(t + gridDim.x, nxt);
+        } else if (kFast) {
+            load_tile(t, cur);
+        }
         if constexpr (kFast && sizeof(T) == 2) {
             // bf16: min and max on packed bf16x2 words (both are exact on bf16
             // values), carried through the butterfly as one (min, -max) pair
-            uint4 q[kU];
-            const T* src = x + n * p.D + (g0 + gw) * kG + lane * 8;
-#pragma unroll
-            for (int u = 0; u < kU; ++u)
-                if (gw + u < gcount) q[u] = ldg_nc_u4(src + u * kG);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 if (gw + u < gcount) {
                     float mn, mx;
-                    warp_minmax_bf16(q[u], mn, mx);
+                    warp_minmax_bf16(cur[u][0], mn, mx);
                     if (lane == u) {
                         myMn = mn;
                         myMx = mx;
@@ -88,10 +104,8 @@ __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) 
             }
         } else if (kFast) {
             float v[kU][8];
-            const T* src = x + n * p.D + (g0 + gw) * kG + lane * 8;
 #pragma unroll
-            for (int u = 0; u < kU; ++u)
-                if (gw + u < gcount) load8(src + u * kG, v[u]);
+            for (int u = 0; u < kU; ++u) raw8_f32<T>(cur[u], v[u]);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 if (gw + u < gcount) {
@@ -152,6 +166,13 @@ __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) 
             if (lane == 0) p.T[c * p.N + n] = v;  // chunk-major: coalesced in K1b
         }
         __syncthreads();
+        if (kFast && ACTNN_K1_PREFETCH) {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                cur[u][0] = nxt[u][0];
+                cur[u][1] = nxt[u][1];
+            }
+        }
     }
     // K1b fused: the last CTA sums every sample's chunk partials in order.
     __shared__ unsigned int s_last;
