@@ -23,6 +23,9 @@ namespace {
 #ifndef ACTNN_K1_PREFETCH
 #define ACTNN_K1_PREFETCH 0  // 1: next tile in flight; measured slower (74 registers, 3 CTAs/SM)
 #endif
+#ifndef ACTNN_K1_U32
+#define ACTNN_K1_U32 4
+#endif
 #ifndef ACTNN_K1_U16
 #define ACTNN_K1_U16 4
 #endif
@@ -30,7 +33,7 @@ template <typename T>
 struct SCfg {
     // groups per warp: 4 (4 KB fp32 / 2 KB bf16 in flight); 8 bf16 groups per
     // warp measured 8% slower on the largest C4 tensor (fewer CTAs per SM)
-    static constexpr int U = sizeof(T) == 2 ? ACTNN_K1_U16 : 4;
+    static constexpr int U = sizeof(T) == 2 ? ACTNN_K1_U16 : ACTNN_K1_U32;
     static constexpr int Block = (kChunk / U) * 32;
 };
 constexpr unsigned kFull = 0xffffffffu;
