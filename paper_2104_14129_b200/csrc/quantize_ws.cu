@@ -52,6 +52,9 @@ namespace {
 #ifndef ACTNN_WS_CWAIT
 #define ACTNN_WS_CWAIT mbar_wait
 #endif
+#ifndef ACTNN_WS_SWP
+#define ACTNN_WS_SWP 1
+#endif
 #ifndef ACTNN_WS_NARROW_ST
 #define ACTNN_WS_NARROW_ST 1
 #endif
@@ -205,6 +208,42 @@ __device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_
                                              const Rel& rel) {
     constexpr int U = WS<T>::U;
     constexpr int PH = WS<T>::PH;
+#if ACTNN_WS_SWP
+    // software-pipelined: the Philox draws of batch h + PH are computed in the
+    // same straight-line block as the codes and stores of batch h, so the
+    // FMA-heavy (IMAD.WIDE) and ALU instruction streams interleave
+    Philox4 o[PH];
+#pragma unroll
+    for (int q = 0; q < PH; ++q) o[q] = philox4x32_10_c32((uint32_t)(blk + (uint64_t)(q * 32)), rk);
+#pragma unroll
+    for (int h = 0; h < U; h += PH) {
+        float v[PH][8];
+        float Z[PH], inv[PH];
+#pragma unroll
+        for (int q = 0; q < PH; ++q) {
+            lds8(st + (h + q) * kG + lane * 8, v[q]);
+            Z[q] = d.Z[h + q];
+            inv[q] = d.inv[h + q];
+        }
+        if (h + PH >= U) {
+            __syncwarp();
+            if (lane == 0) rel();
+        }
+        Philox4 on[PH];
+        if (h + PH < U) {
+#pragma unroll
+            for (int q = 0; q < PH; ++q)
+                on[q] = philox4x32_10_c32((uint32_t)(blk + (uint64_t)((h + PH + q) * 32)), rk);
+        }
+#pragma unroll
+        for (int q = 0; q < PH; ++q)
+            ws_store<b>(v[q], Z[q], inv[q], o[q], seg + (h + q) * 32 * b, lane);
+        if (h + PH < U) {
+#pragma unroll
+            for (int q = 0; q < PH; ++q) o[q] = on[q];
+        }
+    }
+#else
 #pragma unroll
     for (int h = 0; h < U; h += PH) {
         float v[PH][8];
@@ -229,6 +268,7 @@ __device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_
         for (int q = 0; q < PH; ++q)
             ws_store<b>(v[q], Z[q], inv[q], o[q], seg + (h + q) * 32 * b, lane);
     }
+#endif
 }
 
 template <typename T, typename Rel>
