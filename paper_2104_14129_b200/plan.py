@@ -161,13 +161,16 @@ class ActivationSetPlan:
         return self._evs
 
     def compress_all(self, main: torch.cuda.Stream, side: torch.cuda.Stream,
-                     alloc: Optional[torch.cuda.Stream] = None):
+                     alloc: Optional[torch.cuda.Stream] = None,
+                     quant2: Optional[torch.cuda.Stream] = None):
         """Compress every tensor, software-pipelined over streams: the stats
         kernels run back to back on `side`; tensor l's [all-gather ->]
         allocation runs on `alloc` (high priority) once its stats are done, and
         `main` quantises tensor l once its allocation is done.  The single-CTA
         allocator and every kernel's ramp-up/tail overlap other tensors' work.
-        Every output is ready on `main` on return."""
+        With `quant2`, the quantisations alternate between `main` and `quant2`
+        (one tensor's tail overlaps the next one's ramp-up, as in
+        decompress_all).  Every output is ready on `main` on return."""
         if not self.mixed:
             sp = _P(main.cuda_stream)
             for i in range(len(self.layers)):
@@ -178,7 +181,7 @@ class ActivationSetPlan:
             self._evs2 = [(torch.cuda.Event(), torch.cuda.Event()) for _ in self.layers]
         alloc = alloc if alloc is not None else side
         side.wait_stream(main)
-        ss, sa, sm = (_P(side.cuda_stream), _P(alloc.cuda_stream), _P(main.cuda_stream))
+        ss, sa = _P(side.cuda_stream), _P(alloc.cuda_stream)
         for i, L in enumerate(self.layers):
             ev_stats, ev_alloc = self._evs2[i]
             _lib.check(lib.actnn_group_stats(*L.args["stats"], ss))
@@ -190,9 +193,15 @@ class ActivationSetPlan:
                     self.gather(L.S, L.S_loc)
             _lib.check(lib.actnn_allocate_bits(*L.args["alloc"], sa))
             ev_alloc.record(alloc)
+        qs = [main] if quant2 is None else [main, quant2]
+        if quant2 is not None:
+            quant2.wait_stream(main)
+        sps = [_P(q.cuda_stream) for q in qs]
         for i, L in enumerate(self.layers):
-            main.wait_event(self._evs2[i][1])
-            _lib.check(self.qfn(*L.args["quant"], sm))
+            qs[i % len(qs)].wait_event(self._evs2[i][1])
+            _lib.check(self.qfn(*L.args["quant"], sps[i % len(qs)]))
+        if quant2 is not None:
+            main.wait_stream(quant2)
 
     def decompress_all(self, outs: Sequence[torch.Tensor], out_dt: int,
                        streams: Sequence[torch.cuda.Stream]):
