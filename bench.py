@@ -364,6 +364,8 @@ def main():
     aux = torch.cuda.Stream(dev)                  # second decompress stream
     # second quantise stream (consecutive tensors' K3 overlap); ACTNN_Q2=0: one stream
     q2 = torch.cuda.Stream(dev) if os.environ.get("ACTNN_Q2", "1") != "0" else None
+    # second statistics stream (consecutive tensors' K1 overlap); ACTNN_S2=1 enables
+    side2 = torch.cuda.Stream(dev) if os.environ.get("ACTNN_S2", "1") != "0" else None
 
     phase_ev = []   # (start, mid, end) per step: compress / decompress split
     flags = {"phases": False}
@@ -374,7 +376,7 @@ def main():
             if record_phases:
                 marks = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 marks[0].record(stream)
-            plan.compress_all(stream, side, alloc_s, q2)
+            plan.compress_all(stream, side, alloc_s, q2, side2)
             if record_phases:
                 marks[1].record(stream)
             plan.decompress_all(outs, out_dt, [stream, aux])
@@ -415,7 +417,7 @@ def main():
             ref_bits = [L.bits.clone() for L in plan.layers] if dist_on else None
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
-                plan.compress_all(stream, side, alloc_s, q2)
+                plan.compress_all(stream, side, alloc_s, q2, side2)
                 plan.decompress_all(outs, out_dt, [stream, aux])
             if dist_on:  # the replay must redo the exchange: clear S, compare the widths
                 for L in plan.layers:

@@ -162,7 +162,8 @@ class ActivationSetPlan:
 
     def compress_all(self, main: torch.cuda.Stream, side: torch.cuda.Stream,
                      alloc: Optional[torch.cuda.Stream] = None,
-                     quant2: Optional[torch.cuda.Stream] = None):
+                     quant2: Optional[torch.cuda.Stream] = None,
+                     side2: Optional[torch.cuda.Stream] = None):
         """Compress every tensor, software-pipelined over streams: the stats
         kernels run back to back on `side`; tensor l's [all-gather ->]
         allocation runs on `alloc` (high priority) once its stats are done, and
@@ -180,13 +181,17 @@ class ActivationSetPlan:
         if getattr(self, "_evs2", None) is None:
             self._evs2 = [(torch.cuda.Event(), torch.cuda.Event()) for _ in self.layers]
         alloc = alloc if alloc is not None else side
-        side.wait_stream(main)
-        ss, sa = _P(side.cuda_stream), _P(alloc.cuda_stream)
+        sides = [side] if side2 is None or alloc is side else [side, side2]
+        for st in sides:
+            st.wait_stream(main)
+        ss = [_P(st.cuda_stream) for st in sides]
+        sa = _P(alloc.cuda_stream)
         for i, L in enumerate(self.layers):
             ev_stats, ev_alloc = self._evs2[i]
-            _lib.check(lib.actnn_group_stats(*L.args["stats"], ss))
+            st = sides[i % len(sides)]
+            _lib.check(lib.actnn_group_stats(*L.args["stats"], ss[i % len(sides)]))
             if alloc is not side:
-                ev_stats.record(side)
+                ev_stats.record(st)
                 alloc.wait_event(ev_stats)
             if self.gather is not None:
                 with torch.cuda.stream(alloc):
