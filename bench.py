@@ -352,7 +352,9 @@ def main():
                              meta=args.meta,
                              level_mask=0x116 if args.levels == "pow2" else 0x1FE)
     max_numel = max(x.numel() for x in xs)
-    outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(2)]
+    # decompress streams (ACTNN_DQ_STREAMS, default 3) and one output buffer each
+    n_dq = max(1, int(os.environ.get("ACTNN_DQ_STREAMS", "3")))
+    outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(max(2, n_dq))]
     out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
     stream = torch.cuda.Stream(dev)   # main stream (non-default so it can be captured)
     torch.cuda.set_stream(stream)
@@ -362,10 +364,15 @@ def main():
     side = torch.cuda.Stream(dev)                 # stats chain
     alloc_s = torch.cuda.Stream(dev, priority=-1) # per-tensor allocation (high priority)
     aux = torch.cuda.Stream(dev)                  # second decompress stream
+    dq_streams = [stream, aux] + [torch.cuda.Stream(dev) for _ in range(n_dq - 2)]
+    dq_streams = dq_streams[:n_dq]
     # second quantise stream (consecutive tensors' K3 overlap); ACTNN_Q2=0: one stream
-    q2 = torch.cuda.Stream(dev) if os.environ.get("ACTNN_Q2", "1") != "0" else None
-    # second statistics stream (consecutive tensors' K1 overlap); ACTNN_S2=1 enables
-    side2 = torch.cuda.Stream(dev) if os.environ.get("ACTNN_S2", "1") != "0" else None
+    # extra quantise / statistics streams: consecutive tensors' K3 (K1) overlap
+    # (ACTNN_Q_STREAMS / ACTNN_S_STREAMS = total streams, default 2 each)
+    q2 = [torch.cuda.Stream(dev)
+          for _ in range(max(1, int(os.environ.get("ACTNN_Q_STREAMS", "2"))) - 1)]
+    side2 = [torch.cuda.Stream(dev)
+             for _ in range(max(1, int(os.environ.get("ACTNN_S_STREAMS", "2"))) - 1)]
 
     phase_ev = []   # (start, mid, end) per step: compress / decompress split
     flags = {"phases": False}
@@ -379,7 +386,7 @@ def main():
             plan.compress_all(stream, side, alloc_s, q2, side2)
             if record_phases:
                 marks[1].record(stream)
-            plan.decompress_all(outs, out_dt, [stream, aux])
+            plan.decompress_all(outs, out_dt, dq_streams)
             if record_phases:
                 marks[2].record(stream)
                 phase_ev.append(marks)
@@ -418,7 +425,7 @@ def main():
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
                 plan.compress_all(stream, side, alloc_s, q2, side2)
-                plan.decompress_all(outs, out_dt, [stream, aux])
+                plan.decompress_all(outs, out_dt, dq_streams)
             if dist_on:  # the replay must redo the exchange: clear S, compare the widths
                 for L in plan.layers:
                     L.S.zero_()
@@ -537,8 +544,8 @@ def main():
                 "algorithmic_bytes_per_launch": alg[dom] / launches_dom,
                 "avg_launch_us": kt[dom] * 1e3 / launches_dom,
                 # the same kernel inside the timed schedule: K4 is the only kernel of
-                # the decompress phase (its launches overlap on two streams)
-                "in_step": {"phase": "decompress (K4 only, 2 streams)",
+                # the decompress phase (its launches overlap on several streams)
+                "in_step": {"phase": f"decompress (K4 only, {len(dq_streams)} streams)",
                             "GBps": alg["dequantize"] / (t_decomp * 1e-3) / 1e9,
                             "frac": alg["dequantize"] / (t_decomp * 1e-3) / 1e9 / peak},
                 "per_kernel": {k: {"ms_per_step": kt[k], "share_of_step": kt[k] / ms_step,

@@ -162,16 +162,16 @@ class ActivationSetPlan:
 
     def compress_all(self, main: torch.cuda.Stream, side: torch.cuda.Stream,
                      alloc: Optional[torch.cuda.Stream] = None,
-                     quant2: Optional[torch.cuda.Stream] = None,
-                     side2: Optional[torch.cuda.Stream] = None):
+                     quant2=None, side2=None):
         """Compress every tensor, software-pipelined over streams: the stats
         kernels run back to back on `side`; tensor l's [all-gather ->]
         allocation runs on `alloc` (high priority) once its stats are done, and
         `main` quantises tensor l once its allocation is done.  The single-CTA
         allocator and every kernel's ramp-up/tail overlap other tensors' work.
-        With `quant2`, the quantisations alternate between `main` and `quant2`
-        (one tensor's tail overlaps the next one's ramp-up, as in
-        decompress_all).  Every output is ready on `main` on return."""
+        `quant2` / `side2` (a stream or a list of streams): the quantisations /
+        statistics alternate over main + quant2 / side + side2, so one tensor's
+        tail overlaps the next one's ramp-up, as in decompress_all.  Every
+        output is ready on `main` on return."""
         if not self.mixed:
             sp = _P(main.cuda_stream)
             for i in range(len(self.layers)):
@@ -181,7 +181,10 @@ class ActivationSetPlan:
         if getattr(self, "_evs2", None) is None:
             self._evs2 = [(torch.cuda.Event(), torch.cuda.Event()) for _ in self.layers]
         alloc = alloc if alloc is not None else side
-        sides = [side] if side2 is None or alloc is side else [side, side2]
+        def as_list(v):
+            return [] if v is None else (list(v) if isinstance(v, (list, tuple)) else [v])
+
+        sides = [side] if alloc is side else [side] + as_list(side2)
         for st in sides:
             st.wait_stream(main)
         ss = [_P(st.cuda_stream) for st in sides]
@@ -198,15 +201,15 @@ class ActivationSetPlan:
                     self.gather(L.S, L.S_loc)
             _lib.check(lib.actnn_allocate_bits(*L.args["alloc"], sa))
             ev_alloc.record(alloc)
-        qs = [main] if quant2 is None else [main, quant2]
-        if quant2 is not None:
-            quant2.wait_stream(main)
+        qs = [main] + as_list(quant2)
+        for q in qs[1:]:
+            q.wait_stream(main)
         sps = [_P(q.cuda_stream) for q in qs]
         for i, L in enumerate(self.layers):
             qs[i % len(qs)].wait_event(self._evs2[i][1])
             _lib.check(self.qfn(*L.args["quant"], sps[i % len(qs)]))
-        if quant2 is not None:
-            main.wait_stream(quant2)
+        for q in qs[1:]:
+            main.wait_stream(q)
 
     def decompress_all(self, outs: Sequence[torch.Tensor], out_dt: int,
                        streams: Sequence[torch.cuda.Stream]):
