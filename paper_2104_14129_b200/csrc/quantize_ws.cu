@@ -672,6 +672,18 @@ void launch_ws(WSParams p, int64_t units, cudaStream_t s) {
         const int cap = sms * std::atoi(e);
         if (cap > 0 && grid > cap) grid = cap;
     }
+    // ACTNN_WS_GRID_FRAC (0, 1]: a fraction of the full persistent grid, so that
+    // some SMs hold one K3 CTA and can co-host a stats CTA of another tensor
+    static const double frac = [] {
+        const char* e = std::getenv("ACTNN_WS_GRID_FRAC");
+        const double f = e ? std::atof(e) : 1.0;
+        return (f > 0.0 && f < 1.0) ? f : 1.0;
+    }();
+    if (frac < 1.0) {
+        const int full = grid_for(k, kThreads, ws_smem_bytes<T>(), 1ll << 40);
+        const int cap = (int)(full * frac);
+        if (cap >= 1 && grid > cap) grid = cap;
+    }
     const uint32_t nwarps = (uint32_t)grid * kCons;
     p.step_n = nwarps / p.nb;
     p.step_j = nwarps % p.nb;
