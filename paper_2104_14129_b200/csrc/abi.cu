@@ -78,6 +78,18 @@ std::mutex g_dev_mu;
 std::vector<DeviceInfo> g_dev;
 }  // namespace
 
+void ensure_smem_attr(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;  // (kernel, device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : done)
+        if (e.first == kernel && e.second == dev) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done.emplace_back(kernel, dev);
+}
+
 int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks) {
     int dev = 0;
     cudaGetDevice(&dev);

@@ -327,11 +327,7 @@ __global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(const __grid
 template <typename TO, bool kCached, bool kMeta, bool kB16>
 void launch_fast(const DParams& p0, int64_t units, cudaStream_t s) {
     const void* k = (const void*)dequantize_fast_kernel<TO, kCached, kMeta, kB16>;
-    static bool attr = false;  // one-time opt-in above 48 KB of dynamic smem
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-        attr = true;
-    }
+    ensure_smem_attr(k, kSmem);  // opt-in above 48 KB of dynamic smem
     DParams p = p0;
     const int grid = grid_for(k, kBlock, kSmem, (units + kWarps - 1) / kWarps);
     const uint32_t nwarps = (uint32_t)grid * kWarps;

@@ -135,4 +135,8 @@ cudaError_t launch_uniform_bits(int64_t N, int b, int64_t unit, uint8_t* bits, i
 // persistent-grid sizing: min(work, SMs * resident blocks per SM)
 int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks);
 
+// Opt `kernel` into `bytes` of dynamic shared memory on the current device, once
+// per (kernel, device) (thread-safe; several GPUs in one process are fine).
+void ensure_smem_attr(const void* kernel, size_t bytes);
+
 }  // namespace actnn

@@ -450,12 +450,7 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
         const bool cached = a.N <= kNCap;
         const void* k = cached ? (const void*)quantize_fast_kernel<T, kStats, true>
                                : (const void*)quantize_fast_kernel<T, kStats, false>;
-        static bool attr[2] = {false, false};  // one-time opt-in above 48 KB of dynamic smem
-        if (!attr[cached]) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem_bytes<T>());
-            attr[cached] = true;
-        }
+        ensure_smem_attr(k, smem_bytes<T>());  // opt-in above 48 KB of dynamic smem
         const int64_t units = a.N * nb;
         const int grid = grid_for(k, kBlock, smem_bytes<T>(), (units + kWarps - 1) / kWarps);
         const uint32_t nwarps = (uint32_t)grid * kWarps;

@@ -656,12 +656,7 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
 template <typename T, bool kCached>
 void launch_ws(WSParams p, int64_t units, cudaStream_t s) {
     const void* k = (const void*)quantize_ws_kernel<T, kCached>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)ws_smem_bytes<T>());
-        attr = true;
-    }
+    ensure_smem_attr(k, ws_smem_bytes<T>());
     int grid = grid_for(k, kThreads, ws_smem_bytes<T>(), (units + kCons - 1) / kCons);
     // ACTNN_WS_CTAS_PER_SM caps the persistent grid (tuning: leaves room on every
     // SM for a concurrently running stats kernel of the next tensor)
