@@ -16,6 +16,7 @@
 // the windows that contain it in increasing output order (no atomics, so the
 // fp32 sum order is fixed and equals the oracle's / PyTorch CPU's).
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "launch.h"
@@ -381,6 +382,79 @@ __global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_kernel(const uint8_t*
     }
 }
 
+// Row-sliding backward of the ResNet max pool (3x3, stride 2, padding 1): a
+// warp owns 32 consecutive output columns of one plane and walks its window
+// rows; window row i + 1 is loaded once and reused as row i of the next step,
+// column j + 1 comes from the neighbouring lane by a shuffle.  No divisions in
+// the loop (the per-output forward kernel measured equal to a row-sliding one).
+// backward: lane = output column j = input columns 2j, 2j+1; rows of windows i
+// (current) and i + 1 (next) give input rows 2i, 2i+1 exactly as in
+// maxpool_bwd_k3s2_kernel (same taps, same accumulation order)
+template <typename T>
+__global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_rows(const uint8_t* __restrict__ idx,
+                                                                const T* __restrict__ gy, Pool g,
+                                                                T* __restrict__ gx) {
+    const int H = (int)g.H, W = (int)g.W, OH = (int)g.OH, OW = (int)g.OW;
+    const int BH = (H + 1) >> 1, BW = (W + 1) >> 1;
+    const int lane = threadIdx.x & 31;
+    const int nchunk = (BW + 31) >> 5;
+    const int64_t strips = g.NC * nchunk;
+    const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t sw = (((int64_t)blockIdx.x * kBlock) + threadIdx.x) >> 5; sw < strips; sw += nw) {
+        const int64_t p = sw / nchunk;
+        const int j = (int)(sw - p * nchunk) * 32 + lane;
+        const uint8_t* __restrict__ ipl = idx + p * g.OH * g.OW;
+        const T* __restrict__ gpl = gy + p * g.OH * g.OW;
+        T* __restrict__ out = gx + p * g.H * g.W;
+        // window row w: (k, g) at columns j and j + 1 (absent windows: tap 255)
+        auto load_wrow = [&](int w, int& k0, float& g0, int& k1, float& g1) {
+            const bool wok = w < OH;
+            k0 = (wok && j < OW) ? (int)__ldg(ipl + w * OW + j) : 255;
+            g0 = (wok && j < OW) ? widen1(gpl, (int64_t)w * OW + j) : 0.0f;
+            int kn = __shfl_down_sync(0xffffffffu, k0, 1);
+            float gn = __shfl_down_sync(0xffffffffu, g0, 1);
+            if (lane == 31) {
+                kn = (wok && j + 1 < OW) ? (int)__ldg(ipl + w * OW + j + 1) : 255;
+                gn = (wok && j + 1 < OW) ? widen1(gpl, (int64_t)w * OW + j + 1) : 0.0f;
+            }
+            k1 = (j + 1 < OW) ? kn : 255;
+            g1 = gn;
+        };
+        int k00, k01, k10, k11;
+        float g00, g01, g10, g11;
+        load_wrow(0, k00, g00, k01, g01);
+        for (int i = 0; i < BH; ++i) {
+            load_wrow(i + 1, k10, g10, k11, g11);
+            if (j < BW) {
+                const int r = 2 * i, c = 2 * j;
+                float a00 = 0.0f;
+                if (k00 == 4) a00 += g00;
+                float a01 = 0.0f;
+                if (k00 == 5) a01 += g00;
+                if (k01 == 3) a01 += g01;
+                float a10 = 0.0f;
+                if (k00 == 7) a10 += g00;
+                if (k10 == 1) a10 += g10;
+                float a11 = 0.0f;
+                if (k00 == 8) a11 += g00;
+                if (k01 == 6) a11 += g01;
+                if (k10 == 2) a11 += g10;
+                if (k11 == 0) a11 += g11;
+                store_acc(out + (int64_t)r * W + c, a00);
+                if (c + 1 < W) store_acc(out + (int64_t)r * W + c + 1, a01);
+                if (r + 1 < H) {
+                    store_acc(out + (int64_t)(r + 1) * W + c, a10);
+                    if (c + 1 < W) store_acc(out + (int64_t)(r + 1) * W + c + 1, a11);
+                }
+            }
+            k00 = k10;
+            g00 = g10;
+            k01 = k11;
+            g01 = g11;
+        }
+    }
+}
+
 bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
 
 template <typename T>
@@ -439,7 +513,17 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
     const int by = (int)std::min<int64_t>(a.NC, 65535);
     const bool k3s2 = a.kh == 3 && a.kw == 3 && a.sh == 2 && a.sw == 2 && a.ph == 1 &&
                       a.pw == 1 && a.dh == 1 && a.dw == 1;
-    if (!backward && k3s2) {
+    static const bool rows = [] {  // ACTNN_POOL_ROWS=0: the 2x2-block backward
+        const char* e = std::getenv("ACTNN_POOL_ROWS");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (k3s2 && rows && backward) {
+        const int64_t per = backward ? ((a.W + 1) / 2 + 31) / 32 : (a.OW + 31) / 32;
+        const int64_t warps = a.NC * per;
+        const int grid = grid_for((const void*)maxpool_bwd_k3s2_rows<T>, kBlock, 0, (warps + 7) / 8);
+        maxpool_bwd_k3s2_rows<T><<<grid, kBlock, 0, s>>>(a.idx, static_cast<const T*>(a.in), g,
+                                                          static_cast<T*>(a.out));
+    } else if (!backward && k3s2) {
         maxpool_fwd_k3s2_kernel<T><<<dim3(bx, by), kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
                                                                   static_cast<T*>(a.out), a.idx);
     } else if (!backward) {
