@@ -10,6 +10,10 @@
 
 namespace actnn {
 
+#ifndef ACTNN_REDUX_F32
+#define ACTNN_REDUX_F32 1
+#endif
+
 constexpr int kG = 256;            // group size ("we set G = 256")
 constexpr int kWarp = 32;
 constexpr int kElemsPerLane = 8;   // kG / kWarp: one Philox call per lane per group
@@ -152,9 +156,17 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
 // Group (min, max) of 8 bf16 values per lane (four bf16x2 words) over the
 // warp: min and -max travel as one bf16x2 pair through the butterfly (both
 // exact on bf16 values); returns them widened to fp32.
+__device__ __forceinline__ float warp_min(float v);
+__device__ __forceinline__ float warp_max(float v);
 __device__ __forceinline__ void warp_minmax_bf16(uint4 w, float& mn, float& mx) {
     const uint32_t mn2 = bmin2(bmin2(w.x, w.y), bmin2(w.z, w.w));
     const uint32_t mx2 = bmax2(bmax2(w.x, w.y), bmax2(w.z, w.w));
+#if ACTNN_REDUX_F32
+    // the lane's min / max widened (exact), then one warp reduction each
+    mn = warp_min(fminf(__uint_as_float(mn2 << 16), __uint_as_float(mn2 & 0xFFFF0000u)));
+    mx = warp_max(fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xFFFF0000u)));
+    return;
+#endif
     const uint32_t nmx2 = mx2 ^ 0x80008000u;  // -max, exact
     uint32_t r = bmin2(__byte_perm(mn2, nmx2, 0x5410), __byte_perm(mn2, nmx2, 0x7632));
 #pragma unroll
@@ -163,15 +175,31 @@ __device__ __forceinline__ void warp_minmax_bf16(uint4 w, float& mn, float& mx) 
     mx = __uint_as_float((r & 0xFFFF0000u) ^ 0x80000000u);
 }
 
+// Warp-wide min / max of fp32 values (exact selections; signed zeros are
+// canonicalised by the callers).  sm_100a has a one-instruction warp reduction
+// for f32 min/max (redux.sync -> CREDUX, result in a uniform register) in place
+// of five shuffle + compare steps.
 __device__ __forceinline__ float warp_min(float v) {
+#if ACTNN_REDUX_F32
+    float r;
+    asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+#else
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+#endif
 }
 __device__ __forceinline__ float warp_max(float v) {
+#if ACTNN_REDUX_F32
+    float r;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+#else
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+#endif
 }
 
 // ---------------------------------------------------------------- loads
