@@ -12,6 +12,8 @@
 //   K1b: S_n = ((0 + T_{n,0}) + T_{n,1}) + ... in chunk order, run by the
 //       last CTA to finish (an atomicInc ticket in the workspace that wraps
 //       back to 0, so no reset launch is needed) -- one launch per tensor.
+#include <cstdlib>
+
 #include "device.cuh"
 #include "launch.h"
 
@@ -198,7 +200,22 @@ cudaError_t run(const StatsArgs& a, cudaStream_t s) {
               reinterpret_cast<unsigned int*>(a.T + a.N * a.nch)};
     const int64_t tiles = a.N * a.nch;
     if (a.fast) {
-        const int grid = grid_for((const void*)group_stats_kernel<T, true>, SCfg<T>::Block, 0, tiles);
+        int grid = grid_for((const void*)group_stats_kernel<T, true>, SCfg<T>::Block, 0, tiles);
+        // fp32: a persistent grid of 4 CTAs (32 warps) per SM measured best (the
+        // occupancy limit, 8, is 2-4% slower on large tensors); bf16 keeps the
+        // occupancy limit (4 per SM is 11% slower there).  ACTNN_K1_CTAS_PER_SM
+        // overrides (0: occupancy limit).
+        static const int env_cap = [] {
+            const char* e = std::getenv("ACTNN_K1_CTAS_PER_SM");
+            return e ? std::atoi(e) : -1;
+        }();
+        const int cap_per_sm = env_cap >= 0 ? env_cap : (sizeof(T) == 4 ? 4 : 0);
+        if (cap_per_sm > 0) {
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (grid > sms * cap_per_sm) grid = sms * cap_per_sm;
+        }
         group_stats_kernel<T, true><<<grid, SCfg<T>::Block, 0, s>>>(p);
     } else {
         const int grid = grid_for((const void*)group_stats_kernel<T, false>, SCfg<T>::Block, 0, tiles);
