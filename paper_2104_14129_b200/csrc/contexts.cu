@@ -12,7 +12,9 @@
 // Max pooling (App. B.4): "For each output location y_nij, we
 // need to store an integer value k_nij = argmax ... We use 8 bits per output
 // location."  Forward: thread per output, window max and first argmax tap
-// (row-major a * kw + b).  Backward: thread per input element, a gather over
+// (row-major a * kw + b); for the ResNet stem (3x3, stride 2, pad 1, W a
+// multiple of 8 / 16) one thread per run of 4 (fp32) / 8 (bf16) outputs with
+// vector loads (maxpool_fwd_k3s2_vec).  Backward: thread per input element, a gather over
 // the windows that contain it in increasing output order (no atomics, so the
 // fp32 sum order is fixed and equals the oracle's / PyTorch CPU's).
 #include <algorithm>
@@ -25,6 +27,12 @@ namespace actnn {
 namespace {
 
 constexpr int kBlock = 256;
+#ifndef ACTNN_POOL_K32  // outputs per thread of the vector k3s2 forward (fp32 / bf16);
+#define ACTNN_POOL_K32 4  // 8 measured 15% slower for fp32, 4 for bf16 18% slower
+#endif
+#ifndef ACTNN_POOL_K16
+#define ACTNN_POOL_K16 8
+#endif
 
 template <typename T>
 struct RV;  // elements per 256-bit access
@@ -324,6 +332,113 @@ __global__ void __launch_bounds__(kBlock) maxpool_fwd_k3s2_kernel(const T* __res
     }
 }
 
+// Forward, W % (2K) == 0 (every ResNet stem): one thread per K adjacent
+// outputs (i, Km) .. (i, Km+K-1), whose windows cover columns 2Km-1 .. 2Km+2K-1
+// of rows 2i-1 .. 2i+1 -- per row aligned vector loads of columns 2Km ..
+// 2Km+2K-1 plus the scalar 2Km-1 (an L1 hit: the neighbouring thread's
+// vector), 3 (K/2 + 1) loads for K outputs instead of 9 K.  The taps are
+// scanned in the same (a, b) order with the same strict ">" as above, so values
+// and first-index ties are unchanged.  K = 4 (bf16: one 16-byte load per row,
+// fp32: two).
+template <typename T, int K>
+__device__ __forceinline__ void ld_cols(const T* p, float (&v)[2 * K]) {
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int q = 0; q < K / 2; ++q) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(p) + q);
+            v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(p) + q);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                v[8 * q + 2 * h] = __uint_as_float(w[h] << 16);
+                v[8 * q + 2 * h + 1] = __uint_as_float(w[h] & 0xFFFF0000u);
+            }
+        }
+    }
+}
+template <typename T, int K>
+__device__ __forceinline__ void st_outs(T* p, const float (&b)[K]) {
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int q = 0; q < K / 4; ++q)
+            reinterpret_cast<float4*>(p)[q] = make_float4(b[4 * q], b[4 * q + 1], b[4 * q + 2], b[4 * q + 3]);
+    } else {  // exact: the b are bf16 values
+        uint32_t w[K / 2];
+#pragma unroll
+        for (int h = 0; h < K / 2; ++h)
+            w[h] = (__float_as_uint(b[2 * h]) >> 16) | (__float_as_uint(b[2 * h + 1]) & 0xFFFF0000u);
+        if constexpr (K == 8)
+            *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+        else if constexpr (K == 4)
+            *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+        else
+            *reinterpret_cast<uint32_t*>(p) = w[0];
+    }
+}
+template <typename T>
+constexpr int kPoolK = sizeof(T) == 2 ? ACTNN_POOL_K16 : ACTNN_POOL_K32;
+
+// flat grid-stride over (plane, row, run): a plane's 56 x 14 runs do not fill
+// whole CTAs, so planes share CTAs (32-bit indices; the launcher checks range)
+template <typename T>
+__global__ void __launch_bounds__(kBlock) maxpool_fwd_k3s2_vec(const T* __restrict__ x, Pool g,
+                                                               T* __restrict__ y,
+                                                               uint8_t* __restrict__ idx) {
+    constexpr int K = kPoolK<T>;
+    const int H = (int)g.H, W = (int)g.W, OW = (int)g.OW;
+    const uint32_t M = (uint32_t)OW / K;  // output runs per row (OW = W / 2)
+    const uint32_t Q = (uint32_t)g.OH * M;
+    const uint32_t total = (uint32_t)g.NC * Q;
+    for (uint32_t f = blockIdx.x * kBlock + threadIdx.x; f < total; f += gridDim.x * kBlock) {
+        {
+            const uint32_t p = f / Q;
+            const uint32_t q = f - p * Q;
+            const int i = (int)(q / M);
+            const int m = (int)(q - i * M);
+            const T* __restrict__ plane = x + (size_t)p * H * W;
+            float best[K];
+            int arg[K];
+#pragma unroll
+            for (int t = 0; t < K; ++t) best[t] = 0.0f, arg[t] = -1;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int r = 2 * i - 1 + a;
+                if (r < 0 || r >= H) continue;
+                const T* row = plane + r * W + 2 * K * m;
+                float v[2 * K];
+                ld_cols<T, K>(row, v);
+                // column 2Km-1 by a scalar load (an L1 hit); taking it from the
+                // previous lane by a shuffle measured 3-5% slower
+                const float left = m > 0 ? widen1(row, -1) : 0.0f;
+#pragma unroll
+                for (int t = 0; t < K; ++t) {
+                    // output Km + t: columns 2(Km+t) - 1, 2(Km+t), 2(Km+t) + 1
+                    if (t > 0 || m > 0) {
+                        const float l = t > 0 ? v[2 * t - 1] : left;
+                        if (arg[t] < 0 || l > best[t]) best[t] = l, arg[t] = a * 3;
+                    }
+                    if (arg[t] < 0 || v[2 * t] > best[t]) best[t] = v[2 * t], arg[t] = a * 3 + 1;
+                    if (v[2 * t + 1] > best[t]) best[t] = v[2 * t + 1], arg[t] = a * 3 + 2;
+                }
+            }
+            const size_t o = (size_t)p * (g.OH * g.OW) + i * OW + K * m;
+            st_outs<T, K>(y + o, best);
+            uint32_t packed[K / 4] = {};
+#pragma unroll
+            for (int t = 0; t < K; ++t) packed[t / 4] |= (uint32_t)arg[t] << (8 * (t % 4));
+            if constexpr (K == 8)
+                *reinterpret_cast<uint2*>(idx + o) = make_uint2(packed[0], packed[1]);
+            else
+                *reinterpret_cast<uint32_t*>(idx + o) = packed[0];
+        }
+    }
+}
+
 // Backward: one thread per 2x2 block of inputs (rows 2i, 2i+1; columns 2j,
 // 2j+1), which are covered only by the windows (i, j), (i, j+1), (i+1, j),
 // (i+1, j+1): input (2i+s, 2j+t) takes tap a = 1 + s (window row i) or a = 0
@@ -517,12 +632,25 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
         const char* e = std::getenv("ACTNN_POOL_ROWS");
         return !e || std::atoi(e) != 0;
     }();
+    static const bool vec_fwd = [] {  // ACTNN_POOL_VEC=0: the one-output-per-thread forward
+        const char* e = std::getenv("ACTNN_POOL_VEC");
+        return !e || std::atoi(e) != 0;
+    }();
     if (k3s2 && rows && backward) {
         const int64_t per = backward ? ((a.W + 1) / 2 + 31) / 32 : (a.OW + 31) / 32;
         const int64_t warps = a.NC * per;
         const int grid = grid_for((const void*)maxpool_bwd_k3s2_rows<T>, kBlock, 0, (warps + 7) / 8);
         maxpool_bwd_k3s2_rows<T><<<grid, kBlock, 0, s>>>(a.idx, static_cast<const T*>(a.in), g,
                                                           static_cast<T*>(a.out));
+    } else if (!backward && k3s2 && a.W % (2 * kPoolK<T>) == 0 && vec_fwd &&
+               a.NC * a.OH * (a.OW / kPoolK<T>) < (1ll << 32) - kBlock * 65536ll &&
+               reinterpret_cast<uintptr_t>(a.in) % (2 * kPoolK<T> * sizeof(T)) == 0 &&
+               reinterpret_cast<uintptr_t>(a.out) % (kPoolK<T> * sizeof(T)) == 0 &&
+               reinterpret_cast<uintptr_t>(a.idx) % kPoolK<T> == 0) {
+        const int64_t runs = a.NC * a.OH * (a.OW / kPoolK<T>);
+        const int gv = grid_for((const void*)maxpool_fwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
+        maxpool_fwd_k3s2_vec<T><<<gv, kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
+                                                                static_cast<T*>(a.out), a.idx);
     } else if (!backward && k3s2) {
         maxpool_fwd_k3s2_kernel<T><<<dim3(bx, by), kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
                                                                   static_cast<T*>(a.out), a.idx);

@@ -77,6 +77,10 @@ GEOMS = [  # (N, C, H, W, kernel, stride, padding, dilation)
     (2, 3, 112, 112, (3, 3), (2, 2), (1, 1), (1, 1)),
     (2, 3, 13, 15, (3, 3), (2, 2), (1, 1), (1, 1)),   # odd sizes: the 2x2-block edges
     (1, 2, 8, 7, (3, 3), (2, 2), (1, 1), (1, 1)),
+    (1, 2, 13, 16, (3, 3), (2, 2), (1, 1), (1, 1)),   # W % 8 == 0: the vector forward
+    (2, 3, 1, 8, (3, 3), (2, 2), (1, 1), (1, 1)),
+    (1, 2, 6, 24, (3, 3), (2, 2), (1, 1), (1, 1)),
+    (1, 3, 7, 32, (3, 3), (2, 2), (1, 1), (1, 1)),
     (1, 1, 2, 3, (3, 3), (2, 2), (1, 1), (1, 1)),
     (2, 5, 13, 17, (2, 2), (2, 2), (0, 0), (1, 1)),
     (1, 4, 15, 15, (3, 3), (1, 1), (1, 1), (2, 2)),
