@@ -14,7 +14,9 @@
 // location."  Forward: thread per output, window max and first argmax tap
 // (row-major a * kw + b); for the ResNet stem (3x3, stride 2, pad 1, W a
 // multiple of 8 / 16) one thread per run of 4 (fp32) / 8 (bf16) outputs with
-// vector loads (maxpool_fwd_k3s2_vec).  Backward: thread per input element, a gather over
+// vector loads (maxpool_fwd_k3s2_vec); the backward likewise by runs
+// (maxpool_bwd_k3s2_vec), the row-sliding / per-block kernels being the
+// fallbacks for other widths.  Backward: thread per input element, a gather over
 // the windows that contain it in increasing output order (no atomics, so the
 // fp32 sum order is fixed and equals the oracle's / PyTorch CPU's).
 #include <algorithm>
@@ -361,20 +363,23 @@ __device__ __forceinline__ void ld_cols(const T* p, float (&v)[2 * K]) {
         }
     }
 }
-template <typename T, int K>
+template <typename T, int K, bool kRound = false>
 __device__ __forceinline__ void st_outs(T* p, const float (&b)[K]) {
     if constexpr (sizeof(T) == 4) {
 #pragma unroll
         for (int q = 0; q < K / 4; ++q)
             reinterpret_cast<float4*>(p)[q] = make_float4(b[4 * q], b[4 * q + 1], b[4 * q + 2], b[4 * q + 3]);
-    } else {  // exact: the b are bf16 values
+    } else {  // !kRound: exact, the b are bf16 values (forward)
         uint32_t w[K / 2];
 #pragma unroll
         for (int h = 0; h < K / 2; ++h)
-            w[h] = (__float_as_uint(b[2 * h]) >> 16) | (__float_as_uint(b[2 * h + 1]) & 0xFFFF0000u);
-        if constexpr (K == 8)
-            *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
-        else if constexpr (K == 4)
+            w[h] = kRound ? pack_bf16x2(b[2 * h], b[2 * h + 1])  // RNE, as store_acc
+                          : (__float_as_uint(b[2 * h]) >> 16) | (__float_as_uint(b[2 * h + 1]) & 0xFFFF0000u);
+        if constexpr (K % 8 == 0) {
+#pragma unroll
+            for (int q = 0; q < K / 8; ++q)
+                reinterpret_cast<uint4*>(p)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        } else if constexpr (K == 4)
             *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
         else
             *reinterpret_cast<uint32_t*>(p) = w[0];
@@ -494,6 +499,95 @@ __global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_kernel(const uint8_t*
                 if (c + 1 < W) store_acc(out + (r + 1) * W + c + 1, a11);
             }
         }
+    }
+}
+
+// Vector backward of the ResNet max pool (W a multiple of 2K): one thread per
+// (plane, block row i, run m of K output columns), i.e. input rows 2i, 2i+1 and
+// columns 2Km .. 2Km+2K-1, read from window rows i, i+1 at columns Km .. Km+K
+// (column Km+K: a scalar load, L1 hit) with vector idx / grad loads, written
+// with vector stores.  Taps and accumulation order as maxpool_bwd_k3s2_kernel.
+template <typename T, int K>
+__device__ __forceinline__ void ld_idx(const uint8_t* p, int (&k)[K]) {
+    uint32_t w[K / 4];
+    if constexpr (K == 8) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+        w[0] = u.x, w[1] = u.y;
+    } else {
+        w[0] = __ldg(reinterpret_cast<const uint32_t*>(p));
+    }
+#pragma unroll
+    for (int t = 0; t < K; ++t) k[t] = (int)((w[t / 4] >> (8 * (t % 4))) & 0xFFu);
+}
+#ifndef ACTNN_POOLB_K32
+#define ACTNN_POOLB_K32 4  // fp32 runs of 8 measured 15% slower
+#endif
+template <typename T>
+constexpr int kPoolKB = sizeof(T) == 2 ? ACTNN_POOL_K16 : ACTNN_POOLB_K32;
+template <typename T>
+__global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_vec(const uint8_t* __restrict__ idx,
+                                                               const T* __restrict__ gy, Pool g,
+                                                               T* __restrict__ gx) {
+    constexpr int K = kPoolKB<T>;
+    const int H = (int)g.H, W = (int)g.W, OH = (int)g.OH, OW = (int)g.OW;
+    const uint32_t BH = (uint32_t)(H + 1) >> 1;
+    const uint32_t M = (uint32_t)OW / K;
+    const uint32_t Q = BH * M;
+    const uint32_t total = (uint32_t)g.NC * Q;
+    for (uint32_t f = blockIdx.x * kBlock + threadIdx.x; f < total; f += gridDim.x * kBlock) {
+        const uint32_t p = f / Q;
+        const uint32_t q = f - p * Q;
+        const int i = (int)(q / M);
+        const int m = (int)(q - i * M);
+        const uint8_t* __restrict__ ipl = idx + (size_t)p * OH * OW;
+        const T* __restrict__ gpl = gy + (size_t)p * OH * OW;
+        // window rows i (c = 0) and i + 1 (c = 1), columns Km .. Km+K (tap 255: absent)
+        int k[2][K + 1];
+        float gv[2][K + 1];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int w = i + c;
+            if (w < OH) {
+                const int o = w * OW + K * m;
+                ld_idx<T, K>(ipl + o, *reinterpret_cast<int(*)[K]>(&k[c][0]));
+                float tmp[K];
+                ld_cols<T, K / 2>(gpl + o, tmp);
+#pragma unroll
+                for (int t = 0; t < K; ++t) gv[c][t] = tmp[t];
+                if (m + 1 < (int)M) {
+                    k[c][K] = (int)__ldg(ipl + o + K);
+                    gv[c][K] = widen1(gpl, o + K);
+                } else {
+                    k[c][K] = 255, gv[c][K] = 0.0f;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t <= K; ++t) k[c][t] = 255, gv[c][t] = 0.0f;
+            }
+        }
+        float top[2 * K], bot[2 * K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            const int k00 = k[0][t], k01 = k[0][t + 1], k10 = k[1][t], k11 = k[1][t + 1];
+            const float g00 = gv[0][t], g01 = gv[0][t + 1], g10 = gv[1][t], g11 = gv[1][t + 1];
+            float a00 = 0.0f;
+            if (k00 == 4) a00 += g00;
+            float a01 = 0.0f;
+            if (k00 == 5) a01 += g00;
+            if (k01 == 3) a01 += g01;
+            float a10 = 0.0f;
+            if (k00 == 7) a10 += g00;
+            if (k10 == 1) a10 += g10;
+            float a11 = 0.0f;
+            if (k00 == 8) a11 += g00;
+            if (k01 == 6) a11 += g01;
+            if (k10 == 2) a11 += g10;
+            if (k11 == 0) a11 += g11;
+            top[2 * t] = a00, top[2 * t + 1] = a01, bot[2 * t] = a10, bot[2 * t + 1] = a11;
+        }
+        T* __restrict__ out = gx + (size_t)p * H * W + (size_t)(2 * i) * W + 2 * K * m;
+        st_outs<T, 2 * K, true>(out, top);
+        if (2 * i + 1 < H) st_outs<T, 2 * K, true>(out + W, bot);
     }
 }
 
@@ -632,11 +726,20 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
         const char* e = std::getenv("ACTNN_POOL_ROWS");
         return !e || std::atoi(e) != 0;
     }();
-    static const bool vec_fwd = [] {  // ACTNN_POOL_VEC=0: the one-output-per-thread forward
+    static const bool vec_fwd = [] {  // ACTNN_POOL_VEC=0: the scalar k3s2 forward and backward
         const char* e = std::getenv("ACTNN_POOL_VEC");
         return !e || std::atoi(e) != 0;
     }();
-    if (k3s2 && rows && backward) {
+    if (k3s2 && backward && a.W % (2 * kPoolKB<T>) == 0 && vec_fwd &&
+        a.NC * ((a.H + 1) / 2) * (a.OW / kPoolKB<T>) < (1ll << 32) - kBlock * 65536ll &&
+        reinterpret_cast<uintptr_t>(a.in) % (kPoolKB<T> * sizeof(T)) == 0 &&
+        reinterpret_cast<uintptr_t>(a.out) % (2 * kPoolKB<T> * sizeof(T)) == 0 &&
+        reinterpret_cast<uintptr_t>(a.idx) % kPoolKB<T> == 0) {
+        const int64_t runs = a.NC * ((a.H + 1) / 2) * (a.OW / kPoolKB<T>);
+        const int gv = grid_for((const void*)maxpool_bwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
+        maxpool_bwd_k3s2_vec<T><<<gv, kBlock, 0, s>>>(a.idx, static_cast<const T*>(a.in), g,
+                                                     static_cast<T*>(a.out));
+    } else if (k3s2 && rows && backward) {
         const int64_t per = backward ? ((a.W + 1) / 2 + 31) / 32 : (a.OW + 31) / 32;
         const int64_t warps = a.NC * per;
         const int grid = grid_for((const void*)maxpool_bwd_k3s2_rows<T>, kBlock, 0, (warps + 7) / 8);
