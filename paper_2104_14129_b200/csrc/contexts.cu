@@ -714,6 +714,15 @@ cudaError_t relu_backward_t(const ReluArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ACTNN_POOL_FULLGRID: 1 one thread per run, 0 a persistent grid, unset the default
+int pool_full_grid() {
+    static const int v = [] {
+        const char* e = std::getenv("ACTNN_POOL_FULLGRID");
+        return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+
 template <typename T>
 cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
     Pool g{a.NC, a.H, a.W, a.OH, a.OW, a.kh, a.kw, a.sh, a.sw, a.ph, a.pw, a.dh, a.dw};
@@ -736,7 +745,11 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
         reinterpret_cast<uintptr_t>(a.out) % (2 * kPoolKB<T> * sizeof(T)) == 0 &&
         reinterpret_cast<uintptr_t>(a.idx) % kPoolKB<T> == 0) {
         const int64_t runs = a.NC * ((a.H + 1) / 2) * (a.OW / kPoolKB<T>);
-        const int gv = grid_for((const void*)maxpool_bwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
+        // one thread per run (all runs in flight) for fp32, +16% over a persistent
+        // grid; bf16 keeps the persistent grid (6% better there)
+        const bool full = pool_full_grid() >= 0 ? pool_full_grid() != 0 : sizeof(T) == 4;
+        const int gv = full ? (int)((runs + kBlock - 1) / kBlock)
+                            : grid_for((const void*)maxpool_bwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
         maxpool_bwd_k3s2_vec<T><<<gv, kBlock, 0, s>>>(a.idx, static_cast<const T*>(a.in), g,
                                                      static_cast<T*>(a.out));
     } else if (k3s2 && rows && backward) {
@@ -751,7 +764,9 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
                reinterpret_cast<uintptr_t>(a.out) % (kPoolK<T> * sizeof(T)) == 0 &&
                reinterpret_cast<uintptr_t>(a.idx) % kPoolK<T> == 0) {
         const int64_t runs = a.NC * a.OH * (a.OW / kPoolK<T>);
-        const int gv = grid_for((const void*)maxpool_fwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
+        const bool full = pool_full_grid() != 0;  // one thread per run: 1-2% over persistent
+        const int gv = full ? (int)((runs + kBlock - 1) / kBlock)
+                            : grid_for((const void*)maxpool_fwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
         maxpool_fwd_k3s2_vec<T><<<gv, kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
                                                                 static_cast<T*>(a.out), a.idx);
     } else if (!backward && k3s2) {
