@@ -666,6 +666,17 @@ __global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_rows(const uint8_t* _
 
 bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
 
+// One warp per 4 KB step (every step's loads in flight at once) instead of a
+// persistent grid: 0.90 -> 1.03 of the measured copy bandwidth on the stem
+// activation (tools/relu_time.py).  ACTNN_RELU_FULLGRID=0: the persistent grid.
+int relu_full_grid() {
+    static const int v = [] {
+        const char* e = std::getenv("ACTNN_RELU_FULLGRID");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 template <typename T>
 cudaError_t relu_pack_t(const ReluArgs& a, cudaStream_t s) {
     constexpr int64_t kStep = 4 * 32 * RV<T>::V;
@@ -677,7 +688,8 @@ cudaError_t relu_pack_t(const ReluArgs& a, cudaStream_t s) {
     if (steps > 0) {
         const void* k = a.y ? (const void*)relu_pack_kernel<T, true>
                             : (const void*)relu_pack_kernel<T, false>;
-        const int grid = grid_for(k, kBlock, 0, (steps + kBlock / 32 - 1) / (kBlock / 32));
+        const int64_t wb = (steps + kBlock / 32 - 1) / (kBlock / 32);
+        const int grid = relu_full_grid() > 0 ? (int)std::min<int64_t>(wb, 1 << 30) : grid_for(k, kBlock, 0, wb);
         if (a.y)
             relu_pack_kernel<T, true><<<grid, kBlock, 0, s>>>(x, steps, a.mask, y);
         else
@@ -701,8 +713,9 @@ cudaError_t relu_backward_t(const ReluArgs& a, cudaStream_t s) {
     const bool vec = aligned32(a.x) && aligned32(a.y) && ((uintptr_t)a.mask % sizeof(T)) == 0;
     const int64_t steps = vec ? a.E / kStep : 0;
     if (steps > 0) {
-        const int grid = grid_for((const void*)relu_backward_kernel<T>, kBlock, 0,
-                                  (steps + kBlock / 32 - 1) / (kBlock / 32));
+        const int64_t wb = (steps + kBlock / 32 - 1) / (kBlock / 32);
+        const int grid = relu_full_grid() > 0 ? (int)std::min<int64_t>(wb, 1 << 30)
+                                              : grid_for((const void*)relu_backward_kernel<T>, kBlock, 0, wb);
         relu_backward_kernel<T><<<grid, kBlock, 0, s>>>(a.mask, gy, steps, gx);
     }
     const int64_t e_begin = steps * kStep;
