@@ -132,3 +132,30 @@ def test_maxpool_resnet_stem_full_size_sampled(A):
                                       (2, 2), (1, 1))
         assert np.array_equal(host_bits(gx[n:n + 1, c:c + 1]), gx_ref.view(np.uint32))
     assert torch.allclose(gx.double().sum(), gy.double().sum(), rtol=1e-9, atol=1e-3)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_maxpool_unaligned_views(A, dtype):
+    """Inputs one element off the vector alignment take the scalar k3s2 kernels;
+    their outputs equal the vector kernels' (aligned inputs) and the oracle's."""
+    N, C, H, W = 2, 3, 14, 32
+    g = torch.Generator(device=DEV).manual_seed(7)
+    buf = torch.randint(-4, 5, (N * C * H * W + 1,), generator=g, device=DEV).to(dtype)
+    x_al = buf[:-1].view(N, C, H, W).clone()
+    x_un = buf[1:].view(N, C, H, W)
+    x_un.copy_(x_al)
+    y_a, i_a = A.maxpool2d(x_al, 3, 2, 1)
+    y_u, i_u = A.maxpool2d(x_un, 3, 2, 1)
+    gbuf = torch.randn(y_a.numel() + 1, generator=g, device=DEV).to(dtype)
+    gy_al = gbuf[:-1].view(y_a.shape).clone()
+    gy_un = gbuf[1:].view(y_a.shape)
+    gy_un.copy_(gy_al)
+    gx_a = A.maxpool2d_backward(i_a, gy_al, H, W, 3, 2, 1)
+    gx_u = A.maxpool2d_backward(i_a, gy_un, H, W, 3, 2, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(i_a, i_u) and np.array_equal(host_bits(y_a), host_bits(y_u))
+    assert np.array_equal(host_bits(gx_a), host_bits(gx_u))
+    y_ref, idx_ref = O.maxpool2d_forward(to_oracle(x_al), (3, 3), (2, 2), (1, 1))
+    assert np.array_equal(i_a.cpu().numpy(), idx_ref)
+    gx_ref = O.maxpool2d_backward(idx_ref, to_oracle(gy_al), H, W, (3, 3), (2, 2), (1, 1))
+    assert np.array_equal(host_bits(gx_a), gx_ref.view(host_bits(gx_a).dtype))
