@@ -261,7 +261,8 @@ actnn_status_t actnn_relu_backward(const uint8_t* mask, const void* grad_y, actn
  * padding ph <= kh/2, pw <= kw/2 (padded taps never win), dilation dh, dw >= 1,
  * floor mode: OH = (H + 2 ph - dh (kh - 1) - 1) / sh + 1, OW likewise.
  * y [NC, OH, OW] = window maximum; idx [NC, OH, OW] u8 = first argmax tap
- * a*kw + b in row-major window order (PyTorch's tie rule). */
+ * a*kw + b in row-major window order (PyTorch's tie rule).  x finite: a NaN
+ * tap gives an unspecified (but memory-safe) result. */
 actnn_status_t actnn_maxpool2d_forward(const void* x, actnn_dtype_t dt, int64_t NC, int64_t H,
                                        int64_t W, int32_t kh, int32_t kw, int32_t sh,
                                        int32_t sw, int32_t ph, int32_t pw, int32_t dh,

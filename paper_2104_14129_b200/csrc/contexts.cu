@@ -502,6 +502,114 @@ __global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_kernel(const uint8_t*
     }
 }
 
+// bf16 forward on packed halves (runs of 8 outputs, W a multiple of 16).  Word
+// q of a row holds columns (16m + 2q, 16m + 2q + 1), i.e. taps b = 1, 2 of
+// output t = q, and its high half is tap b = 0 of output q + 1.  The window
+// max is reduced column-wise with max.bf16x2 over the valid rows, then over the
+// three columns; the first argmax tap (row-major, as the scalar kernels) is
+// found by testing every tap for equality with the max (setp.eq.bf16x2: two
+// predicates per word) in reverse tap order, so the earliest match is written
+// last.  The stored value is the max's bits -- except for a max of zero, where
+// the first equal tap's sign of zero is the oracle's; that rare case takes the
+// scalar scan.
+__device__ __forceinline__ void eq_row(int& arg, uint32_t w, uint32_t wl, uint32_t mm, int a3) {
+    // reverse order: b = 2 (hi of w), b = 1 (lo of w), b = 0 (hi of wl)
+    asm("{\n\t.reg .pred l1, h1, l0, h0;\n\t"
+        "setp.eq.bf16x2 l1|h1, %1, %3;\n\t"
+        "setp.eq.bf16x2 l0|h0, %2, %3;\n\t"
+        "@h1 mov.u32 %0, %6;\n\t"
+        "@l1 mov.u32 %0, %5;\n\t"
+        "@h0 mov.u32 %0, %4;\n\t}"
+        : "+r"(arg)
+        : "r"(w), "r"(wl), "r"(mm), "r"(a3), "r"(a3 + 1), "r"(a3 + 2));
+}
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__global__ void __launch_bounds__(kBlock) maxpool_fwd_k3s2_bf16x2(const uint16_t* __restrict__ x,
+                                                                  Pool g, uint16_t* __restrict__ y,
+                                                                  uint8_t* __restrict__ idx) {
+    constexpr int K = 8;
+    constexpr uint32_t kNaN = 0x7FC07FC0u;  // never equal: absent taps
+    const int H = (int)g.H, W = (int)g.W, OW = (int)g.OW;
+    const uint32_t M = (uint32_t)OW / K;
+    const uint32_t Q = (uint32_t)g.OH * M;
+    const uint32_t total = (uint32_t)g.NC * Q;
+    for (uint32_t f = blockIdx.x * kBlock + threadIdx.x; f < total; f += gridDim.x * kBlock) {
+        const uint32_t p = f / Q;
+        const uint32_t q = f - p * Q;
+        const int i = (int)(q / M);
+        const int m = (int)(q - i * M);
+        const uint16_t* __restrict__ plane = x + (size_t)p * H * W;
+        // rows 2i-1, 2i, 2i+1: row 2i always exists (i < OH)
+        const bool v0 = i > 0, v2 = 2 * i + 1 < H;
+        uint32_t w[3][K], L[3];  // L: left column 16m - 1 in the high half (NaN if absent)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const bool rv = a == 1 || (a == 0 ? v0 : v2);
+            const uint16_t* row = plane + (2 * i - 1 + a) * W + 2 * K * m;
+            if (rv) {
+                const uint4 u0 = __ldg(reinterpret_cast<const uint4*>(row));
+                const uint4 u1 = __ldg(reinterpret_cast<const uint4*>(row) + 1);
+                w[a][0] = u0.x, w[a][1] = u0.y, w[a][2] = u0.z, w[a][3] = u0.w;
+                w[a][4] = u1.x, w[a][5] = u1.y, w[a][6] = u1.z, w[a][7] = u1.w;
+                L[a] = m > 0 ? ((uint32_t)row[-1] << 16) | 0x7FC0u : kNaN;
+            } else {
+#pragma unroll
+                for (int t = 0; t < K; ++t) w[a][t] = kNaN;
+                L[a] = kNaN;
+            }
+        }
+        // column maxima over the valid rows (max.bf16x2 drops a NaN operand)
+        uint32_t c[K], cl;
+#pragma unroll
+        for (int t = 0; t < K; ++t) c[t] = bmax2(bmax2(w[0][t], w[1][t]), w[2][t]);
+        cl = bmax2(bmax2(L[0], L[1]), L[2]);
+        float best[K];
+        int arg[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            const uint32_t left = t > 0 ? c[t - 1] : cl;  // tap b = 0 in the high half
+            float mx = fmaxf(__uint_as_float(c[t] << 16), __uint_as_float(c[t] & 0xFFFF0000u));
+            if (t > 0 || m > 0) mx = fmaxf(mx, __uint_as_float(left & 0xFFFF0000u));
+            const uint32_t mb = __float_as_uint(mx) >> 16;
+            const uint32_t mm = mb | (mb << 16);
+            int k = 255;
+#pragma unroll
+            for (int a = 2; a >= 0; --a) eq_row(k, w[a][t], t > 0 ? w[a][t - 1] : L[a], mm, 3 * a);
+            if (mx == 0.0f) {  // sign of zero: the first zero tap's (scalar scan)
+                float b = 0.0f;
+                uint32_t bits = 0;
+                int kk = -1;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const bool rv = a == 1 || (a == 0 ? v0 : v2);
+                    if (!rv) continue;
+                    const uint32_t tw = t > 0 ? w[a][t - 1] : L[a];
+                    const uint32_t h[3] = {tw >> 16, w[a][t] & 0xFFFFu, w[a][t] >> 16};
+#pragma unroll
+                    for (int bb = 0; bb < 3; ++bb) {
+                        if (bb == 0 && t == 0 && m == 0) continue;
+                        const float v = __uint_as_float(h[bb] << 16);
+                        if (kk < 0 || v > b) b = v, bits = h[bb], kk = 3 * a + bb;
+                    }
+                }
+                mx = __uint_as_float(bits << 16);
+            }
+            best[t] = mx;
+            arg[t] = k;
+        }
+        const size_t o = (size_t)p * (g.OH * g.OW) + i * OW + K * m;
+        st_outs<uint16_t, K>(y + o, best);
+        uint32_t packed[2] = {0u, 0u};
+#pragma unroll
+        for (int t = 0; t < K; ++t) packed[t / 4] |= (uint32_t)arg[t] << (8 * (t % 4));
+        *reinterpret_cast<uint2*>(idx + o) = make_uint2(packed[0], packed[1]);
+    }
+}
+
 // Vector backward of the ResNet max pool (W a multiple of 2K): one thread per
 // (plane, block row i, run m of K output columns), i.e. input rows 2i, 2i+1 and
 // columns 2Km .. 2Km+2K-1, read from window rows i, i+1 at columns Km .. Km+K
@@ -780,6 +888,17 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
         const bool full = pool_full_grid() != 0;  // one thread per run: 1-2% over persistent
         const int gv = full ? (int)((runs + kBlock - 1) / kBlock)
                             : grid_for((const void*)maxpool_fwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
+        static const bool packed = [] {  // ACTNN_POOL_PACKED=0: the float-compare bf16 forward
+            const char* e = std::getenv("ACTNN_POOL_PACKED");
+            return !e || std::atoi(e) != 0;
+        }();
+        if constexpr (sizeof(T) == 2) {
+            if (packed && kPoolK<T> == 8) {
+                maxpool_fwd_k3s2_bf16x2<<<gv, kBlock, 0, s>>>(static_cast<const uint16_t*>(a.in), g,
+                                                              static_cast<uint16_t*>(a.out), a.idx);
+                return cudaGetLastError();
+            }
+        }
         maxpool_fwd_k3s2_vec<T><<<gv, kBlock, 0, s>>>(static_cast<const T*>(a.in), g,
                                                                 static_cast<T*>(a.out), a.idx);
     } else if (!backward && k3s2) {

@@ -159,3 +159,22 @@ def test_maxpool_unaligned_views(A, dtype):
     assert np.array_equal(i_a.cpu().numpy(), idx_ref)
     gx_ref = O.maxpool2d_backward(idx_ref, to_oracle(gy_al), H, W, (3, 3), (2, 2), (1, 1))
     assert np.array_equal(host_bits(gx_a), gx_ref.view(host_bits(gx_a).dtype))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_maxpool_signed_zero_ties(A, dtype):
+    """Windows whose maximum is a zero of either sign: the stored value is the
+    first zero tap's, bit for bit (the packed bf16 forward's special case)."""
+    N, C, H, W = 2, 2, 16, 32
+    g = torch.Generator(device=DEV).manual_seed(11)
+    choice = torch.randint(0, 3, (N, C, H, W), generator=g, device=DEV)
+    x = torch.where(choice == 0, torch.tensor(-0.0, device=DEV),
+                    torch.where(choice == 1, torch.tensor(0.0, device=DEV),
+                                torch.tensor(-1.0, device=DEV))).to(dtype)
+    y, idx = A.maxpool2d(x, 3, 2, 1)
+    torch.cuda.synchronize()
+    y_ref, idx_ref = O.maxpool2d_forward(to_oracle(x), (3, 3), (2, 2), (1, 1))
+    assert np.array_equal(idx.cpu().numpy(), idx_ref)
+    assert np.array_equal(host_bits(y), y_ref.view(host_bits(y).dtype))
+    neg0 = 0x8000 if dtype == torch.bfloat16 else 0x80000000
+    assert (host_bits(y) == neg0).any() and (host_bits(y) == 0).any()  # both signs of zero win
