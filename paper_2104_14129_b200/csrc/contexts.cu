@@ -528,7 +528,8 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
     asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
     return r;
 }
-__global__ void __launch_bounds__(kBlock) maxpool_fwd_k3s2_bf16x2(const uint16_t* __restrict__ x,
+// 5 CTAs per SM: 48 registers (a bound of 1 lets ptxas take 56, 0.76 -> 0.60)
+__global__ void __launch_bounds__(kBlock, 5) maxpool_fwd_k3s2_bf16x2(const uint16_t* __restrict__ x,
                                                                   Pool g, uint16_t* __restrict__ y,
                                                                   uint8_t* __restrict__ idx) {
     constexpr int K = 8;
@@ -632,8 +633,11 @@ __device__ __forceinline__ void ld_idx(const uint8_t* p, int (&k)[K]) {
 #endif
 template <typename T>
 constexpr int kPoolKB = sizeof(T) == 2 ? ACTNN_POOL_K16 : ACTNN_POOLB_K32;
+// CTAs per SM the register budget must allow: bf16 5 (48 registers; 0.78 ->
+// 0.81 of HBM over the unbounded 52), fp32 7 (32 registers; 0.76 -> 0.80 over
+// the unbounded 36, and a bound of 5 gave 42 registers and 0.74)
 template <typename T>
-__global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_vec(const uint8_t* __restrict__ idx,
+__global__ void __launch_bounds__(kBlock, sizeof(T) == 2 ? 5 : 7) maxpool_bwd_k3s2_vec(const uint8_t* __restrict__ idx,
                                                                const T* __restrict__ gy, Pool g,
                                                                T* __restrict__ gx) {
     constexpr int K = kPoolKB<T>;
