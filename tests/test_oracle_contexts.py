@@ -120,3 +120,19 @@ def test_maxpool_rejects_more_than_256_taps():
     x = np.zeros((1, 1, 40, 40), np.float32)
     with pytest.raises(ValueError):
         O.maxpool2d_forward(x, (17, 16), (1, 1))
+
+
+def test_maxpool_signed_zero_ties_match_torch():
+    """Windows whose maximum is a zero of either sign: the oracle stores the
+    first zero tap (its sign bit included) and its index, as PyTorch's CPU
+    max_pool2d does (update only on a strictly greater value) -- checked bit
+    for bit, since -0 == +0 compares equal."""
+    rng = np.random.default_rng(5)
+    choice = rng.integers(0, 3, size=(2, 3, 16, 18))
+    xa = np.where(choice == 0, np.float32(-0.0), np.where(choice == 1, np.float32(0.0),
+                                                          np.float32(-1.0))).astype(np.float32)
+    y, idx = O.maxpool2d_forward(xa, (3, 3), (2, 2), (1, 1))
+    yt, it = F.max_pool2d(torch.from_numpy(xa), 3, 2, 1, return_indices=True)
+    assert np.array_equal(y.view(np.uint32), yt.numpy().view(np.uint32))
+    bits = y.view(np.uint32)
+    assert (bits == 0x80000000).any() and (bits == 0).any()  # both signs win somewhere
