@@ -293,7 +293,7 @@ def main():
 
     import paper_2104_14129_b200 as A
     from paper_2104_14129_b200 import workloads as W
-    from paper_2104_14129_b200.plan import ActivationSetPlan
+    from paper_2104_14129_b200.plan import ActivationSetPlan, PipelinedStep
 
     # one process per GPU; ACTNN_DIST_BACKEND=gloo is a test mode in which
     # several ranks may share a GPU (NCCL refuses duplicate devices)
@@ -356,40 +356,33 @@ def main():
     n_dq = max(1, int(os.environ.get("ACTNN_DQ_STREAMS", "3")))
     outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(max(2, n_dq))]
     out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
-    stream = torch.cuda.Stream(dev)   # main stream (non-default so it can be captured)
+    # the timed schedule (plan.PipelinedStep): statistics / quantisation alternate
+    # over ACTNN_S_STREAMS / ACTNN_Q_STREAMS streams (default 2 each), so that
+    # consecutive tensors' kernels overlap; allocation on a high-priority stream
+    ps = PipelinedStep(plan, outs, out_dt, dev,
+                       n_stats=int(os.environ.get("ACTNN_S_STREAMS", "2")),
+                       n_quant=int(os.environ.get("ACTNN_Q_STREAMS", "2")), n_dq=n_dq)
+    stream = ps.stream   # main stream (non-default so it can be captured)
     torch.cuda.set_stream(stream)
-    sp =__import__("ctypes").c_void_p(stream.cuda_stream)
+    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
     nl = len(plan.layers)
-
-    side = torch.cuda.Stream(dev)                 # stats chain
-    alloc_s = torch.cuda.Stream(dev, priority=-1) # per-tensor allocation (high priority)
-    aux = torch.cuda.Stream(dev)                  # second decompress stream
-    dq_streams = [stream, aux] + [torch.cuda.Stream(dev) for _ in range(n_dq - 2)]
-    dq_streams = dq_streams[:n_dq]
-    # second quantise stream (consecutive tensors' K3 overlap); ACTNN_Q2=0: one stream
-    # extra quantise / statistics streams: consecutive tensors' K3 (K1) overlap
-    # (ACTNN_Q_STREAMS / ACTNN_S_STREAMS = total streams, default 2 each)
-    q2 = [torch.cuda.Stream(dev)
-          for _ in range(max(1, int(os.environ.get("ACTNN_Q_STREAMS", "2"))) - 1)]
-    side2 = [torch.cuda.Stream(dev)
-             for _ in range(max(1, int(os.environ.get("ACTNN_S_STREAMS", "2"))) - 1)]
+    dq_streams = ps.dq
 
     phase_ev = []   # (start, mid, end) per step: compress / decompress split
     flags = {"phases": False}
 
     def step(ev=None):
-        record_phases = flags["phases"]
-        if ev is None:  # the timed schedule: software pipeline over streams
-            if record_phases:
-                marks = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-                marks[0].record(stream)
-            plan.compress_all(stream, side, alloc_s, q2, side2)
-            if record_phases:
-                marks[1].record(stream)
-            plan.decompress_all(outs, out_dt, dq_streams)
-            if record_phases:
-                marks[2].record(stream)
-                phase_ev.append(marks)
+        if ev is None and not flags["phases"]:
+            ps()          # the timed schedule: graph replay, or the eager pipeline
+            return
+        if ev is None:    # the same schedule, eager, with events at the phase boundary
+            marks = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            marks[0].record(stream)
+            ps.compress()
+            marks[1].record(stream)
+            ps.decompress()
+            marks[2].record(stream)
+            phase_ev.append(marks)
             return
         # breakdown: serial per-tensor launches, an event pair around each kernel
         for i in range(nl):
@@ -409,9 +402,7 @@ def main():
     # ---- optional: capture the whole pipelined step in one CUDA graph (removes
     # the ~430 per-step CPU launches; every kernel still runs on every replay)
     # Seeds are per tensor and fixed across steps in both modes, so a replay does
-    # exactly the work of an eager step.  At N>1 the step holds a collective
-    # (all-gather of S); it stays eager there.
-    graph = None
+    # exactly the work of an eager step.
     graph_error = None
     if args.graph is None:
         # N > 1: the NCCL all-gathers are captured too (tests/test_gpu_parity.py
@@ -421,31 +412,12 @@ def main():
                                     and os.environ.get("ACTNN_DIST_GRAPH", "1") != "0")
     if args.graph:
         try:
-            ref_bits = [L.bits.clone() for L in plan.layers] if dist_on else None
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=stream):
-                plan.compress_all(stream, side, alloc_s, q2, side2)
-                plan.decompress_all(outs, out_dt, dq_streams)
-            if dist_on:  # the replay must redo the exchange: clear S, compare the widths
-                for L in plan.layers:
-                    L.S.zero_()
-                torch.cuda.synchronize()
-            graph.replay()
+            ps.capture(check_exchange=dist_on)
             barrier()
-            if dist_on and not all(torch.equal(L.bits, r) for L, r in zip(plan.layers, ref_bits)):
-                raise RuntimeError("graph replay did not reproduce the eager widths "
-                                   "(captured all-gather not replayed)")
         except Exception as e:  # fall back to the eager schedule
-            graph, graph_error, args.graph = None, f"{type(e).__name__}: {e}"[:200], False
+            ps.graph, graph_error, args.graph = None, f"{type(e).__name__}: {e}"[:200], False
             torch.cuda.synchronize()
             barrier()
-    if graph is not None:
-        eager_step = step
-
-        def step(ev=None):  # noqa: F811
-            if ev is not None or flags["phases"]:
-                return eager_step(ev)
-            graph.replay()
 
     # ---- headline: K steps, one event pair, max over ranks
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

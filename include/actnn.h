@@ -259,7 +259,10 @@ actnn_status_t actnn_relu_backward(const uint8_t* mask, const void* grad_y, actn
  * location").  x [NC, H, W] (NCHW with NC = N*C planes), PyTorch geometry:
  * kernel kh x kw (kh*kw <= 256, else ACTNN_ERR_UNSUPPORTED), stride sh, sw >= 1,
  * padding ph <= kh/2, pw <= kw/2 (padded taps never win), dilation dh, dw >= 1,
- * floor mode: OH = (H + 2 ph - dh (kh - 1) - 1) / sh + 1, OW likewise.
+ * floor mode: OH = (H + 2 ph - dh (kh - 1) - 1) / sh + 1, OW likewise.  Every
+ * window must hold at least one in-bounds tap; a geometry with a window lying
+ * entirely in the padding (possible with dilation > 1) returns
+ * ACTNN_ERR_UNSUPPORTED and launches nothing.
  * y [NC, OH, OW] = window maximum; idx [NC, OH, OW] u8 = first argmax tap
  * a*kw + b in row-major window order (PyTorch's tie rule).  x finite: a NaN
  * tap gives an unspecified (but memory-safe) result. */

@@ -12,8 +12,7 @@ import re
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# ACTNN_LIB_VARIANT: tuning sweeps load an alternative in-tree build (tools/)
-LIB_PATH = os.environ.get("ACTNN_LIB_VARIANT") or os.path.join(_HERE, "libactnn.so")
+LIB_PATH = os.path.join(_HERE, "libactnn.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "actnn.h")
 
 _lib = None

@@ -70,6 +70,28 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
+def _need(t: Optional[torch.Tensor], name: str, dtype: torch.dtype, numel: Optional[int],
+          device: torch.device, at_least: bool = False, optional: bool = False):
+    """Validate a caller-supplied buffer before its pointer reaches the C ABI:
+    a CUDA tensor on `device`, contiguous, of `dtype`, with `numel` elements
+    (or at least that many).  Raises ActnnError(-1) instead of letting a wrong
+    buffer turn into an out-of-bounds device access."""
+    if t is None:
+        if optional:
+            return
+        raise ActnnError(-1, f"{name} is required")
+    if not t.is_cuda or t.device != device:
+        raise ActnnError(-1, f"{name} must be a CUDA tensor on {device} (got {t.device})")
+    if not t.is_contiguous():
+        raise ActnnError(-1, f"{name} must be contiguous")
+    if t.dtype != dtype:
+        raise ActnnError(-1, f"{name} must be {dtype} (got {t.dtype})")
+    if numel is not None:
+        if (t.numel() < numel) if at_least else (t.numel() != numel):
+            raise ActnnError(-1, f"{name} has {t.numel()} elements, expected "
+                                 f"{'at least ' if at_least else ''}{numel}")
+
+
 def packed_bytes(N: int, D: int, bits_host=None) -> int:
     """Bytes of the packed stream: sum_n b_n * ceil(D/G) * G / 8; None = 8-bit bound."""
     arr = None
@@ -112,10 +134,24 @@ class Packed:
             n *= s
         return n
 
-    def nbytes(self) -> int:
-        meta = (4 * self.meta.numel() if self.meta is not None
+    def meta_bytes(self) -> int:
+        return (4 * self.meta.numel() if self.meta is not None
                 else 4 * self.zmin.numel() + 4 * self.scale.numel())
-        return self.packed.numel() + meta + self.bits.numel() + 8 * self.off.numel()
+
+    def payload_bytes(self) -> int:
+        """Bytes of code stream actually used: off[N] - off[0] (one 16-byte
+        device read; the widths live on the device)."""
+        ends = self.off[[0, -1]].cpu()
+        return int(ends[1] - ends[0])
+
+    def nbytes(self) -> int:
+        """Compressed size of the context: used code bytes + metadata + the
+        per-sample widths and offsets (not the allocated capacity)."""
+        return self.payload_bytes() + self.meta_bytes() + self.bits.numel() + 8 * self.off.numel()
+
+    def capacity_bytes(self) -> int:
+        """Allocated bytes (the packed buffer defaults to the 8-bit bound)."""
+        return self.packed.numel() + self.meta_bytes() + self.bits.numel() + 8 * self.off.numel()
 
 
 def group_stats(x: torch.Tensor, sens_out: Optional[torch.Tensor] = None):
@@ -141,13 +177,15 @@ def group_stats(x: torch.Tensor, sens_out: Optional[torch.Tensor] = None):
 def allocate_bits(sens: torch.Tensor, budget: int, D: int, level_mask: int = LEVELS_POW2,
                   gscale: Optional[torch.Tensor] = None):
     """Stage-1 greedy on the device -> (bits u8 [N], off i64 [N+1])."""
-    if not sens.is_cuda or sens.dtype != torch.float64:
+    if not sens.is_cuda:
         raise ActnnError(-1, "sens must be a CUDA fp64 tensor")
     N = sens.numel()
     dev = sens.device
+    _need(sens, "sens", torch.float64, N, dev)
+    _need(gscale, "gscale", torch.float64, N, dev, optional=True)
     bits = torch.empty(N, dtype=torch.uint8, device=dev)
     off = torch.empty(N + 1, dtype=torch.int64, device=dev)
-    _lib.check(_lib.load().actnn_allocate_bits(_ptr(sens.contiguous()), _ptr(gscale), N,
+    _lib.check(_lib.load().actnn_allocate_bits(_ptr(sens), _ptr(gscale), N,
                                                int(budget), level_mask, D, G, _ptr(bits),
                                                _ptr(off), None, 0, _stream(dev)))
     return bits, off
@@ -177,12 +215,23 @@ def quantize(x: torch.Tensor, bits: torch.Tensor, off: torch.Tensor, seed: int,
     N, D = x2.shape
     ng = ceil_div(D, G)
     dev = x2.device
+    _need(bits, "bits", torch.uint8, N, dev)
+    _need(off, "off", torch.int64, N + 1, dev)
+    if (gmin is None) != (gmax is None):
+        raise ActnnError(-1, "give both gmin and gmax (two-pass) or neither (single pass)")
+    _need(gmin, "gmin", torch.float32, N * ng, dev, optional=True)
+    _need(gmax, "gmax", torch.float32, N * ng, dev, optional=True)
     if packed is None:
         nbytes = packed_nbytes if packed_nbytes is not None else N * ng * G
         packed = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    else:
+        # the device-resident widths decide the real size (off[N] - off[0] bytes);
+        # a caller-sized buffer must hold at least packed_nbytes when given
+        _need(packed, "packed", torch.uint8, packed_nbytes, dev, at_least=True)
     if meta == "bf16":
         if meta_out is None:
             meta_out = torch.empty(N * ng, dtype=torch.int32, device=dev)
+        _need(meta_out, "meta_out", torch.int32, N * ng, dev)
         _lib.check(_lib.load().actnn_quantize_bf16meta(
             _ptr(x2), _dtype_code(x2.dtype), N, D, G, _ptr(bits), _ptr(off),
             ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), sample_base, _ptr(gmin), _ptr(gmax),
@@ -195,6 +244,8 @@ def quantize(x: torch.Tensor, bits: torch.Tensor, off: torch.Tensor, seed: int,
         zmin = torch.empty(N * ng, dtype=torch.float32, device=dev)
     if scale is None:
         scale = torch.empty(N * ng, dtype=torch.float32, device=dev)
+    _need(zmin, "zmin", torch.float32, N * ng, dev)
+    _need(scale, "scale", torch.float32, N * ng, dev)
     _lib.check(_lib.load().actnn_quantize(
         _ptr(x2), _dtype_code(x2.dtype), N, D, G, _ptr(bits), _ptr(off),
         ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), sample_base, _ptr(gmin), _ptr(gmax),
@@ -206,8 +257,20 @@ def dequantize(p: Packed, out: Optional[torch.Tensor] = None,
                out_dtype: Optional[torch.dtype] = None) -> torch.Tensor:
     """Decompressor into a tensor of the original shape."""
     dev = p.packed.device
+    N, D = p.N, p.D
+    ng = ceil_div(D, G)
     if out is None:
         out = torch.empty(p.shape, dtype=out_dtype or p.dtype, device=dev)
+    _need(out, "out", out.dtype if out.dtype in (torch.float32, torch.bfloat16) else torch.float32,
+          N * D, dev)
+    _need(p.packed, "packed", torch.uint8, None, dev)
+    _need(p.bits, "bits", torch.uint8, N, dev)
+    _need(p.off, "off", torch.int64, N + 1, dev)
+    if p.meta is not None:
+        _need(p.meta, "meta", torch.int32, N * ng, dev)
+    else:
+        _need(p.zmin, "zmin", torch.float32, N * ng, dev)
+        _need(p.scale, "scale", torch.float32, N * ng, dev)
     if p.meta is not None:
         _lib.check(_lib.load().actnn_dequantize_bf16meta(
             _ptr(p.packed), _ptr(p.meta), _ptr(p.bits), _ptr(p.off), p.N, p.D, G, _ptr(out),
@@ -272,6 +335,9 @@ def relu_pack(x: torch.Tensor, want_y: bool = False):
 
 def relu_backward(mask: torch.Tensor, grad_y: torch.Tensor) -> torch.Tensor:
     grad_y = grad_y.contiguous()
+    if not grad_y.is_cuda:
+        raise ActnnError(-1, "relu_backward needs CUDA tensors")
+    _need(mask, "mask", torch.uint8, (grad_y.numel() + 7) // 8, grad_y.device)
     gx = torch.empty_like(grad_y)
     _lib.check(_lib.load().actnn_relu_backward(_ptr(mask), _ptr(grad_y),
                                                _dtype_code(grad_y.dtype), grad_y.numel(),
@@ -311,7 +377,14 @@ def maxpool2d_backward(idx: torch.Tensor, grad_y: torch.Tensor, H: int, W: int, 
     s = _pair(stride if stride is not None else kernel)
     p, d = _pair(padding), _pair(dilation)
     grad_y = grad_y.contiguous()
+    if not grad_y.is_cuda or grad_y.dim() != 4:
+        raise ActnnError(-1, "maxpool2d_backward needs a CUDA grad_y [N, C, OH, OW]")
     N, C = grad_y.shape[:2]
+    OH, OW = _pool_extent(H, k[0], s[0], p[0], d[0]), _pool_extent(W, k[1], s[1], p[1], d[1])
+    if tuple(grad_y.shape[2:]) != (OH, OW):
+        raise ActnnError(-1, f"grad_y is {tuple(grad_y.shape)}, the pooling geometry gives "
+                             f"[{N}, {C}, {OH}, {OW}]")
+    _need(idx, "idx", torch.uint8, grad_y.numel(), grad_y.device)
     gx = torch.empty((N, C, H, W), dtype=grad_y.dtype, device=grad_y.device)
     _lib.check(_lib.load().actnn_maxpool2d_backward(
         _ptr(idx), _ptr(grad_y), _dtype_code(grad_y.dtype), N * C, H, W, k[0], k[1], s[0], s[1],
@@ -350,6 +423,10 @@ def gradmag_ema(obs: torch.Tensor, m: torch.Tensor, rho: float = 0.9) -> torch.T
 def gradmag_gather(table: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
     """Stale estimator: est[n] = table[ids[n]]."""
     ids = ids.contiguous()
+    if not table.is_cuda:
+        raise ActnnError(-1, "gradmag_gather needs CUDA tensors")
+    _need(table, "table", torch.float64, None, table.device)
+    _need(ids, "ids", torch.int64, None, table.device)
     est = torch.empty(ids.numel(), dtype=torch.float64, device=table.device)
     _lib.check(_lib.load().actnn_gradmag_gather(_ptr(table), table.numel(), _ptr(ids),
                                                 ids.numel(), _ptr(est), _stream(table.device)))
@@ -359,6 +436,11 @@ def gradmag_gather(table: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
 def gradmag_scatter(table: torch.Tensor, ids: torch.Tensor, obs: torch.Tensor) -> torch.Tensor:
     """Stale estimator update: table[ids[n]] = obs[n] (in place)."""
     ids, obs = ids.contiguous(), obs.contiguous()
+    if not table.is_cuda:
+        raise ActnnError(-1, "gradmag_scatter needs CUDA tensors")
+    _need(table, "table", torch.float64, None, table.device)
+    _need(ids, "ids", torch.int64, None, table.device)
+    _need(obs, "obs", torch.float64, ids.numel(), table.device)
     _lib.check(_lib.load().actnn_gradmag_scatter(_ptr(table), table.numel(), _ptr(ids),
                                                  _ptr(obs), ids.numel(), _stream(table.device)))
     return table
@@ -386,6 +468,9 @@ class LayerAllocator:
         sens = sens.contiguous()
         gscale = gscale.contiguous() if gscale is not None else None
         lconst = lconst.contiguous() if lconst is not None else None
+        _need(sens, "sens", torch.float64, self.L * self.N, self.dev)
+        _need(gscale, "gscale", torch.float64, self.L * self.N, self.dev, optional=True)
+        _need(lconst, "lconst", torch.float64, self.L, self.dev, optional=True)
         bits = torch.empty((self.L, self.N), dtype=torch.uint8, device=self.dev)
         budgets = torch.empty(self.L, dtype=torch.int64, device=self.dev)
         _lib.check(_lib.load().actnn_allocate_layers(

@@ -31,14 +31,14 @@ actnn_status_t cuda_status(cudaError_t e, const char* what) {
     return fail(ACTNN_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-bool check_mode() {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* v = std::getenv("ACTNN_CHECK");
-        mode = (v && v[0] && v[0] != '0') ? 1 : 0;
-    }
-    return mode == 1;
-}
+// ACTNN_CHECK is read once, when the library is loaded (the only environment
+// variable the library reads).
+const bool g_check_mode = [] {
+    const char* v = std::getenv("ACTNN_CHECK");
+    return v != nullptr && v[0] != '\0' && v[0] != '0';
+}();
+
+bool check_mode() { return g_check_mode; }
 
 bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -90,21 +90,35 @@ void ensure_smem_attr(const void* kernel, size_t bytes) {
     done.emplace_back(kernel, dev);
 }
 
-int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks) {
+int sm_count() {
     int dev = 0;
     cudaGetDevice(&dev);
-    int sms = 0;
-    {
-        std::lock_guard<std::mutex> lk(g_dev_mu);
-        if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
-        if (g_dev[dev].sms == 0)
-            cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev);
-        sms = g_dev[dev].sms;
-    }
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+    if (g_dev[dev].sms == 0)
+        cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+    return g_dev[dev].sms;
+}
+
+int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks) {
+    const int sms = sm_count();
+    // resident blocks per SM, computed once per (kernel, block, smem)
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int64_t>, int>> occ_cache;
+    const int64_t shape = ((int64_t)block << 32) | (int64_t)smem;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem) != cudaSuccess ||
-        occ < 1)
-        occ = 1;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const auto& e : occ_cache)
+            if (e.first.first == kernel && e.first.second == shape) occ = e.second;
+        if (occ == 0) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem) !=
+                    cudaSuccess ||
+                occ < 1)
+                occ = 1;
+            occ_cache.push_back({{kernel, shape}, occ});
+        }
+    }
     const int64_t cap = (int64_t)sms * occ;
     int64_t g = work_blocks < cap ? work_blocks : cap;
     return (int)(g < 1 ? 1 : g);
@@ -537,6 +551,23 @@ static int64_t pool_extent(int64_t H, int k, int s, int p, int d) {
     return (H + 2 * (int64_t)p - (int64_t)d * (k - 1) - 1) / s + 1;
 }
 
+// Every output window along one axis holds at least one in-bounds tap
+// (o s - p + t d in [0, H) for some tap t).  With dilation > 1 a padded window
+// can miss the input entirely (e.g. k = 2, d = 2, p = 1, H = 1); such
+// geometries are rejected -- PyTorch would return -inf there and no 8-bit tap
+// index could name the winner.
+static bool windows_hit_input(int64_t H, int64_t OH, int k, int s, int p, int d) {
+    for (int64_t o = 0; o < OH; ++o) {
+        bool hit = false;
+        for (int t = 0; t < k && !hit; ++t) {
+            const int64_t i = o * s - p + (int64_t)t * d;
+            hit = i >= 0 && i < H;
+        }
+        if (!hit) return false;
+    }
+    return true;
+}
+
 static actnn_status_t pool_args(const char* fn, actnn_dtype_t dt, int64_t NC, int64_t H,
                                 int64_t W, int32_t kh, int32_t kw, int32_t sh, int32_t sw,
                                 int32_t ph, int32_t pw, int32_t dh, int32_t dw, PoolArgs* a) {
@@ -557,6 +588,8 @@ static actnn_status_t pool_args(const char* fn, actnn_dtype_t dt, int64_t NC, in
     a->OH = pool_extent(H, kh, sh, ph, dh);
     a->OW = pool_extent(W, kw, sw, pw, dw);
     if (a->OH < 1 || a->OW < 1) return fail(ACTNN_ERR_INVALID, "%s: empty output", fn);
+    if (!windows_hit_input(H, a->OH, kh, sh, ph, dh) || !windows_hit_input(W, a->OW, kw, sw, pw, dw))
+        return fail(ACTNN_ERR_UNSUPPORTED, "%s: a pooling window lies entirely in the padding", fn);
     a->kh = kh;
     a->kw = kw;
     a->sh = sh;

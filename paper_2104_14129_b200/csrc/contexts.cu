@@ -780,14 +780,11 @@ bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
 
 // One warp per 4 KB step (every step's loads in flight at once) instead of a
 // persistent grid: 0.90 -> 1.03 of the measured copy bandwidth on the stem
-// activation (tools/relu_time.py).  ACTNN_RELU_FULLGRID=0: the persistent grid.
-int relu_full_grid() {
-    static const int v = [] {
-        const char* e = std::getenv("ACTNN_RELU_FULLGRID");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
+// activation (tools/relu_time.py).  -DACTNN_RELU_FULLGRID=0: the persistent grid.
+#ifndef ACTNN_RELU_FULLGRID
+#define ACTNN_RELU_FULLGRID 1
+#endif
+constexpr int relu_full_grid() { return ACTNN_RELU_FULLGRID; }
 
 template <typename T>
 cudaError_t relu_pack_t(const ReluArgs& a, cudaStream_t s) {
@@ -839,14 +836,24 @@ cudaError_t relu_backward_t(const ReluArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// ACTNN_POOL_FULLGRID: 1 one thread per run, 0 a persistent grid, unset the default
-int pool_full_grid() {
-    static const int v = [] {
-        const char* e = std::getenv("ACTNN_POOL_FULLGRID");
-        return e ? std::atoi(e) : -1;
-    }();
-    return v;
-}
+// Build-time variants (measured; the defaults are the fastest):
+//   ACTNN_POOL_FULLGRID  1 one thread per run, 0 a persistent grid, -1 per dtype
+//   ACTNN_POOL_ROWS      0: the 2x2-block backward instead of the row kernel
+//   ACTNN_POOL_VEC       0: the scalar k3s2 forward and backward
+//   ACTNN_POOL_PACKED    0: the float-compare bf16 forward
+#ifndef ACTNN_POOL_FULLGRID
+#define ACTNN_POOL_FULLGRID -1
+#endif
+#ifndef ACTNN_POOL_ROWS
+#define ACTNN_POOL_ROWS 1
+#endif
+#ifndef ACTNN_POOL_VEC
+#define ACTNN_POOL_VEC 1
+#endif
+#ifndef ACTNN_POOL_PACKED
+#define ACTNN_POOL_PACKED 1
+#endif
+constexpr int pool_full_grid() { return ACTNN_POOL_FULLGRID; }
 
 template <typename T>
 cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
@@ -856,14 +863,8 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
     const int by = (int)std::min<int64_t>(a.NC, 65535);
     const bool k3s2 = a.kh == 3 && a.kw == 3 && a.sh == 2 && a.sw == 2 && a.ph == 1 &&
                       a.pw == 1 && a.dh == 1 && a.dw == 1;
-    static const bool rows = [] {  // ACTNN_POOL_ROWS=0: the 2x2-block backward
-        const char* e = std::getenv("ACTNN_POOL_ROWS");
-        return !e || std::atoi(e) != 0;
-    }();
-    static const bool vec_fwd = [] {  // ACTNN_POOL_VEC=0: the scalar k3s2 forward and backward
-        const char* e = std::getenv("ACTNN_POOL_VEC");
-        return !e || std::atoi(e) != 0;
-    }();
+    constexpr bool rows = ACTNN_POOL_ROWS != 0;
+    constexpr bool vec_fwd = ACTNN_POOL_VEC != 0;
     if (k3s2 && backward && a.W % (2 * kPoolKB<T>) == 0 && vec_fwd &&
         a.NC * ((a.H + 1) / 2) * (a.OW / kPoolKB<T>) < (1ll << 32) - kBlock * 65536ll &&
         reinterpret_cast<uintptr_t>(a.in) % (kPoolKB<T> * sizeof(T)) == 0 &&
@@ -893,10 +894,7 @@ cudaError_t maxpool_t(const PoolArgs& a, bool backward, cudaStream_t s) {
         const bool full = pool_full_grid() >= 0 ? pool_full_grid() != 0 : sizeof(T) == 4;
         const int gv = full ? (int)((runs + kBlock - 1) / kBlock)
                             : grid_for((const void*)maxpool_fwd_k3s2_vec<T>, kBlock, 0, (runs + kBlock - 1) / kBlock);
-        static const bool packed = [] {  // ACTNN_POOL_PACKED=0: the float-compare bf16 forward
-            const char* e = std::getenv("ACTNN_POOL_PACKED");
-            return !e || std::atoi(e) != 0;
-        }();
+        constexpr bool packed = ACTNN_POOL_PACKED != 0;
         if constexpr (sizeof(T) == 2) {
             if (packed && kPoolK<T> == 8) {
                 maxpool_fwd_k3s2_bf16x2<<<gv, kBlock, 0, s>>>(static_cast<const uint16_t*>(a.in), g,

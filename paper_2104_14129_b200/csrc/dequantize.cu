@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
         else if (b == 6) dequant_unit<TO, 6, false>(st, gcount, zq, sq, dst, lane);
         else if (b == 7) dequant_unit<TO, 7, false>(st, gcount, zq, sq, dst, lane);
         // the stage's shared loads were consumed by the stores above: re-arm it
+        // (cross-proxy WAR: each lane's generic loads are ordered before the
+        // async-proxy bulk write by fence.proxy.async, all lanes before lane 0's
+        // issue by the __syncwarp)
+        fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
             if (pn < p.N) issue(pn, pj, stage);

@@ -398,6 +398,35 @@ __device__ __forceinline__ uint32_t codes_small(const float v[8], float Z, float
     return (y | (y >> 15)) & 0xFFu;
 }
 
+// Codes of one lane's 8 elements at b >= 3 (q up to 2^22, one code per
+// element; ACTNN-Q v1 O5-O7).  ACTNN_WIDE_F32X2=1 forms (h - Z) and the fma
+// against 1.5*2^23 two elements at a time with the sm_100 f32x2 instructions
+// (FADD2 / FFMA2: the same IEEE roundings per element as the scalar forms).
+#ifndef ACTNN_WIDE_F32X2
+#define ACTNN_WIDE_F32X2 0
+#endif
+__device__ __forceinline__ void codes_wide(const float v[8], float Z, float inv14,
+                                           const Philox4& o, uint32_t code[8]) {
+    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#if ACTNN_WIDE_F32X2
+    const float2 nz = make_float2(-Z, -Z), iv = make_float2(inv14, inv14),
+                 mg = make_float2(12582912.0f, 12582912.0f);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
+        const float2 t = __ffma2_rn(d, iv, mg);
+        code[2 * p] = (__float_as_uint(t.x) - 0x4B400000u + (w[p] & 0x3FFFu)) >> 14;
+        code[2 * p + 1] = (__float_as_uint(t.y) - 0x4B400000u + ((w[p] >> 16) & 0x3FFFu)) >> 14;
+    }
+#else
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t r = ((j & 1) ? (w[j >> 1] >> 16) : w[j >> 1]) & 0x3FFFu;
+        code[j] = sr_code(v[j], Z, inv14, r);
+    }
+#endif
+}
+
 // ACTNN-Q v1 O10: h_hat = fmaf((float)code, scale, Z); (float)code is exact
 // via the 2^23 magic (code < 2^8).
 __device__ __forceinline__ float dequant1(uint32_t code, float scale, float Z) {

@@ -132,6 +132,9 @@ cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s);
 cudaError_t launch_uniform_bits(int64_t N, int b, int64_t unit, uint8_t* bits, int64_t* off,
                                 cudaStream_t s);
 
+// SM count of the current device (cached per device)
+int sm_count();
+
 // persistent-grid sizing: min(work, SMs * resident blocks per SM)
 int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks);
 

@@ -33,6 +33,10 @@
 namespace actnn {
 namespace {
 
+#ifndef ACTNN_NO_WS
+#define ACTNN_NO_WS 0  // build-time diagnostics: 1 sends the mixed path to this file's kernel
+#endif
+
 constexpr int kU = 4;
 constexpr int kWarps = 8;
 constexpr int kBlock = kWarps * 32;
@@ -130,17 +134,7 @@ __device__ __forceinline__ void group_const_store(float mn, float mx, int b, uin
 
 // Codes for b in {1, 2}: codes_small (device.cuh).
 
-// Codes for b >= 3 (q up to 2^22): one code per element (scalar fp32 ops; the
-// f32x2 form of this variant miscompiled in testing).
-__device__ __forceinline__ void codes_wide(const float v[8], float Z, float inv14,
-                                          const Philox4& o, uint32_t code[8]) {
-    const uint32_t w[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t r = ((j & 1) ? (w[j >> 1] >> 16) : w[j >> 1]) & 0x3FFFu;
-        code[j] = sr_code(v[j], Z, inv14, r);
-    }
-}
+// Codes for b >= 3: codes_wide (device.cuh).
 
 // One group: Philox draw for the lane's 8-element block, SR codes, pack, store
 // (ACTNN-Q v1 O6-O8).  seg = the group's 32 b-byte segment.
@@ -298,9 +292,12 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
         for (int k = 0; k < kU; ++k)
             if (k < gcount) lds8(st + k * kG + lane * 8, v[k]);
         // Re-arm the stage with the unit S ahead as soon as it has been read, so
-        // S units stay in flight while this one is computed.  In-warp WAR: all
-        // lanes issued their shared loads before the __syncwarp; the new bulk
-        // copy first has to fetch from HBM (~1 us) before it writes the stage.
+        // S units stay in flight while this one is computed.  Cross-proxy WAR
+        // (generic-proxy shared loads, then an async-proxy bulk write to the same
+        // bytes): every lane orders its loads before the async proxy with
+        // fence.proxy.async, the __syncwarp orders all lanes before lane 0, and
+        // only then does lane 0 issue the copy into the stage.
+        fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
             if (pn < p.N) {
@@ -494,7 +491,7 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
                       a.sample_base + a.N < (1ll << 31) &&
                       (a.sample_base + a.N) * a.D <= (1ll << 35);
     // mixed path (group stats given): the warp-specialised kernel (quantize_ws.cu)
-    if (!stats && a.fast && fits && !std::getenv("ACTNN_NO_WS")) return launch_quantize_ws(a, s);
+    if (!stats && a.fast && fits && !ACTNN_NO_WS) return launch_quantize_ws(a, s);
     if (a.dt == 0) return stats ? run<float, true>(a, s) : run<float, false>(a, s);
     return stats ? run<uint16_t, true>(a, s) : run<uint16_t, false>(a, s);
 }

@@ -58,6 +58,9 @@ namespace {
 #ifndef ACTNN_WS_NARROW_ST
 #define ACTNN_WS_NARROW_ST 1
 #endif
+#ifndef ACTNN_WS_CTAS_PER_SM
+#define ACTNN_WS_CTAS_PER_SM 0  // 0: the occupancy limit
+#endif
 #ifndef ACTNN_WS_PROD
 #define ACTNN_WS_PROD 2
 #endif
@@ -156,13 +159,8 @@ __device__ __forceinline__ void ws_store(const float v[8], float Z, float inv14,
             *reinterpret_cast<uint32_t*>(seg + lane) = pl | (q1 << 8) | (q2 << 16) | (q3 << 24);
     } else {
 #endif
-        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
         uint32_t code[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t r = ((j & 1) ? (w[j >> 1] >> 16) : w[j >> 1]) & 0x3FFFu;
-            code[j] = sr_code(v[j], Z, inv14, r);
-        }
+        codes_wide(v, Z, inv14, o, code);
         if constexpr (b == 8) {
             const uint32_t lo = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
             const uint32_t hi = code[4] | (code[5] << 8) | (code[6] << 16) | (code[7] << 24);
@@ -556,8 +554,12 @@ __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(co
             if (!__any_sync(kFull, valid)) return false;
             const int s = (int)(r % kS);
             const int slot = c * kS + s;
-            if (r >= (uint32_t)kS && valid && kl == 0)
+            if (r >= (uint32_t)kS && valid && kl == 0) {
                 ACTNN_WS_PWAIT(&empty[slot], ((r / kS) - 1) & 1);
+                // the consumer's generic-proxy reads of this stage (released by its
+                // arrive, acquired by the wait) precede the async-proxy refill
+                fence_proxy_async();
+            }
             __syncwarp();
             const uint32_t gi = j * U;
             const int gcount = (int)min((uint32_t)U, p.ng - gi);
@@ -658,27 +660,10 @@ void launch_ws(WSParams p, int64_t units, cudaStream_t s) {
     const void* k = (const void*)quantize_ws_kernel<T, kCached>;
     ensure_smem_attr(k, ws_smem_bytes<T>());
     int grid = grid_for(k, kThreads, ws_smem_bytes<T>(), (units + kCons - 1) / kCons);
-    // ACTNN_WS_CTAS_PER_SM caps the persistent grid (tuning: leaves room on every
-    // SM for a concurrently running stats kernel of the next tensor)
-    if (const char* e = std::getenv("ACTNN_WS_CTAS_PER_SM")) {
-        int sms = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int cap = sms * std::atoi(e);
-        if (cap > 0 && grid > cap) grid = cap;
-    }
-    // ACTNN_WS_GRID_FRAC (0, 1]: a fraction of the full persistent grid, so that
-    // some SMs hold one K3 CTA and can co-host a stats CTA of another tensor
-    static const double frac = [] {
-        const char* e = std::getenv("ACTNN_WS_GRID_FRAC");
-        const double f = e ? std::atof(e) : 1.0;
-        return (f > 0.0 && f < 1.0) ? f : 1.0;
-    }();
-    if (frac < 1.0) {
-        const int full = grid_for(k, kThreads, ws_smem_bytes<T>(), 1ll << 40);
-        const int cap = (int)(full * frac);
-        if (cap >= 1 && grid > cap) grid = cap;
-    }
+    // -DACTNN_WS_CTAS_PER_SM=k (build-time tuning) caps the persistent grid at k
+    // CTAs per SM, leaving room for a concurrently running stats kernel
+    if (ACTNN_WS_CTAS_PER_SM > 0 && grid > sm_count() * ACTNN_WS_CTAS_PER_SM)
+        grid = sm_count() * ACTNN_WS_CTAS_PER_SM;
     const uint32_t nwarps = (uint32_t)grid * kCons;
     p.step_n = nwarps / p.nb;
     p.step_j = nwarps % p.nb;

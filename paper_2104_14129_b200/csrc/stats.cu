@@ -22,6 +22,9 @@ namespace {
 
 // groups per warp per chunk: 4 (fp32: 4 KB in flight per warp) or 8 (bf16:
 // also 4 KB); a CTA has 32 / U warps so that a chunk is 32 groups.
+#ifndef ACTNN_K1_CTAS_PER_SM
+#define ACTNN_K1_CTAS_PER_SM -1  // -1: 4 per SM at fp32, the occupancy limit at bf16
+#endif
 #ifndef ACTNN_K1_PREFETCH
 #define ACTNN_K1_PREFETCH 0  // 1: next tile in flight; measured slower (74 registers, 3 CTAs/SM)
 #endif
@@ -203,19 +206,11 @@ cudaError_t run(const StatsArgs& a, cudaStream_t s) {
         int grid = grid_for((const void*)group_stats_kernel<T, true>, SCfg<T>::Block, 0, tiles);
         // fp32: a persistent grid of 4 CTAs (32 warps) per SM measured best (the
         // occupancy limit, 8, is 2-4% slower on large tensors); bf16 keeps the
-        // occupancy limit (4 per SM is 11% slower there).  ACTNN_K1_CTAS_PER_SM
-        // overrides (0: occupancy limit).
-        static const int env_cap = [] {
-            const char* e = std::getenv("ACTNN_K1_CTAS_PER_SM");
-            return e ? std::atoi(e) : -1;
-        }();
-        const int cap_per_sm = env_cap >= 0 ? env_cap : (sizeof(T) == 4 ? 4 : 0);
-        if (cap_per_sm > 0) {
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (grid > sms * cap_per_sm) grid = sms * cap_per_sm;
-        }
+        // occupancy limit (4 per SM is 11% slower there).  -DACTNN_K1_CTAS_PER_SM
+        // overrides at build time (0: occupancy limit).
+        const int cap_per_sm = ACTNN_K1_CTAS_PER_SM >= 0 ? ACTNN_K1_CTAS_PER_SM
+                                                         : (sizeof(T) == 4 ? 4 : 0);
+        if (cap_per_sm > 0 && grid > sm_count() * cap_per_sm) grid = sm_count() * cap_per_sm;
         group_stats_kernel<T, true><<<grid, SCfg<T>::Block, 0, s>>>(p);
     } else {
         const int grid = grid_for((const void*)group_stats_kernel<T, false>, SCfg<T>::Block, 0, tiles);

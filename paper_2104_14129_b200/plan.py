@@ -81,6 +81,11 @@ class ActivationSetPlan:
             x2 = x.reshape(x.shape[0], -1)
             N, D = x2.shape
             nt = n_total if n_total is not None else N
+            if self.mixed and nt != N and gather is None:
+                # the global S vector would hold only zeros: the allocation
+                # needs every rank's S_n (the exchange step)
+                raise ValueError("n_total != N (a shard of a larger batch) needs gather= to "
+                                 "exchange the per-sample S_n across ranks")
             ng = ceil_div(D, G)
             dev = x2.device
             dt = F32 if x2.dtype == torch.float32 else BF16
@@ -230,3 +235,68 @@ class ActivationSetPlan:
         lo = self.sample_base
         return [L.bits[lo:lo + L.N].cpu() if L.bits.numel() != L.N else L.bits.cpu()
                 for L in self.layers]
+
+
+class PipelinedStep:
+    """One step of the whole hot path over an ActivationSetPlan -- compress
+    every tensor, then decompress every tensor -- in the schedule bench.py
+    times: statistics alternating over `n_stats` streams, each tensor's
+    [exchange ->] allocation on a high-priority stream, quantisation
+    alternating over `n_quant` streams, decompression over `n_dq` streams
+    (output buffer i % len(outs)).  `capture()` records the step into one CUDA
+    graph (every kernel still runs on each replay); `__call__` replays it, or
+    runs the step eagerly when no graph was captured.  The parity tests build
+    the same object, so what they check is the launch configuration the bench
+    times."""
+
+    def __init__(self, plan: ActivationSetPlan, outs: Sequence[torch.Tensor], out_dt: int,
+                 device=None, n_stats: int = 2, n_quant: int = 2, n_dq: int = 3):
+        self.plan, self.outs, self.out_dt = plan, list(outs), out_dt
+        dev = torch.device(device) if device is not None else plan.layers[0].x.device
+        # main: a non-default stream so that the step can be captured
+        self.stream = torch.cuda.Stream(dev)
+        self.side = torch.cuda.Stream(dev)                    # statistics chain
+        self.alloc = torch.cuda.Stream(dev, priority=-1)      # per-tensor allocation
+        self.side2 = [torch.cuda.Stream(dev) for _ in range(max(1, n_stats) - 1)]
+        self.quant2 = [torch.cuda.Stream(dev) for _ in range(max(1, n_quant) - 1)]
+        self.dq = [self.stream] + [torch.cuda.Stream(dev) for _ in range(max(1, n_dq) - 1)]
+        self.graph = None
+
+    def compress(self):
+        self.plan.compress_all(self.stream, self.side, self.alloc, self.quant2, self.side2)
+
+    def decompress(self):
+        self.plan.decompress_all(self.outs, self.out_dt, self.dq)
+
+    def eager(self):
+        self.compress()
+        self.decompress()
+
+    def capture(self, check_exchange: bool = False):
+        """Capture the step into a CUDA graph and replay it once.  With
+        `check_exchange` (a multi-rank plan), S is cleared before that replay
+        and the replayed widths must equal the eager ones: the captured
+        collectives really ran.  Raises on failure (the caller may fall back
+        to eager steps)."""
+        ref_bits = [L.bits.clone() for L in self.plan.layers] if check_exchange else None
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            self.eager()
+        if check_exchange:
+            for L in self.plan.layers:
+                L.S.zero_()
+            torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        if check_exchange and not all(torch.equal(L.bits, r)
+                                      for L, r in zip(self.plan.layers, ref_bits)):
+            raise RuntimeError("graph replay did not reproduce the eager widths "
+                               "(captured exchange not replayed)")
+        self.graph = g
+
+    def __call__(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            with torch.cuda.stream(self.stream):
+                self.eager()

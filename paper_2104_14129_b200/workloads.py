@@ -180,7 +180,8 @@ def synth_activation(act: Act, N: int, t: int, dtype: str = "f32", device="cpu",
 def adversarial_tensors(rng: np.random.Generator, D: int = 1024):
     """C1-sized tensors exercising the corner cases of the contract
     (SURVEY §8(d)): constant groups, grid-valued groups, negative minima,
-    |Z| >> R, tiny R, signed zeros, subnormals.  Returns {name: [N, D] fp32}."""
+    |Z| >> R, tiny R (degenerate and not), signed zeros, subnormals.
+    Returns {name: [N, D] fp32}."""
     out = {}
     N = 4
     out["constant"] = np.full((N, D), 5.0, np.float32)
@@ -196,6 +197,23 @@ def adversarial_tensors(rng: np.random.Generator, D: int = 1024):
     sub = (rng.random((N, D)) * 2.0 ** -130).astype(np.float32)
     sub[1, :] = np.float32(2.0 ** -100) * rng.random(D).astype(np.float32)
     out["subnormal"] = sub
+    # non-degenerate tiny ranges (SURVEY §8(d) "R in {2^-100, 2^-90}", reading
+    # 16's threshold R < 2^-96): every group spans [0, R] exactly with R = 2^-95,
+    # 2^-90, 2^-96 (the smallest non-degenerate range) and the largest float
+    # below 2^-96 (degenerate: all codes 0); a third of the members are
+    # subnormal, a third normal in (0, R), a third zero, so inv14 is near
+    # B 2^110 and the codes are non-zero
+    tr = np.zeros((N, D), np.float32)
+    k = np.arange(D)
+    for n, R in enumerate((np.float32(2.0 ** -95), np.float32(2.0 ** -90),
+                           np.float32(2.0 ** -96),
+                           np.nextafter(np.float32(2.0 ** -96), np.float32(0)))):
+        u = (rng.random(D) * float(R)).astype(np.float32)
+        s = (rng.random(D) * 2.0 ** -126).astype(np.float32)
+        tr[n] = np.where(k % 3 == 0, u, np.where(k % 3 == 1, s, np.float32(0)))
+        tr[n, 0::G] = 0.0
+        tr[n, 1::G] = R
+    out["tiny_range_nondegenerate"] = tr
     z = np.zeros((N, D), np.float32)
     z[:, 1::2] = -0.0
     z[2, 7] = 1.0

@@ -120,6 +120,10 @@ def test_contexts_host_validation(lib):
     assert fw(d, 0, 4, 112, 112, 3, 3, 0, 2, 1, 1, 1, 1, d, d, None) == INVALID  # stride 0
     assert fw(d, 0, 4, 112, 112, 3, 3, 2, 2, 2, 1, 1, 1, d, d, None) == INVALID  # pad > k/2
     assert fw(d, 0, 4, 2, 2, 5, 5, 1, 1, 0, 0, 1, 1, d, d, None) == INVALID      # empty output
+    # dilation 2, padding 1, a 1-row input: the only window's taps (-1, 1) miss it
+    assert fw(d, 0, 4, 1, 4, 2, 1, 1, 1, 1, 0, 2, 1, d, d, None) == UNSUPPORTED
+    assert "padding" in _msg(lib)
+    assert bw(d, d, 0, 4, 1, 4, 2, 1, 1, 1, 1, 0, 2, 1, d, None) == UNSUPPORTED
     assert fw(None, 0, 0, 112, 112, *geo, None, None, None) == OK
     assert bw(None, d, 0, 4, 112, 112, *geo, d, None) == INVALID
 
@@ -147,6 +151,15 @@ def test_python_binding_refuses_cpu_tensors():
     with pytest.raises(A.ActnnError):
         A.quantize(torch.zeros(4, 1024), torch.zeros(4, dtype=torch.uint8),
                    torch.zeros(5, dtype=torch.int64), 0)
+
+
+def test_plan_shard_without_exchange_is_refused():
+    """A shard of a larger batch (n_total != N) cannot allocate without the
+    exchange of S (the global S would stay all zeros)."""
+    torch = pytest.importorskip("torch")
+    from paper_2104_14129_b200.plan import ActivationSetPlan
+    with pytest.raises(ValueError, match="gather"):
+        ActivationSetPlan([torch.zeros(4, 1024)], [1], avg_bits=2.0, n_total=8, sample_base=4)
 
 
 def test_adaptation_host_validation(lib):

@@ -422,3 +422,46 @@ def test_philox_counter_high_word(A, sample_base, two_pass):
     for bits in ([1, 2, 4, 8], [2, 2, 2, 2]):
         p, ref = run_both(A, x, bits, seed=77, sample_base=sample_base, two_pass=two_pass)
         assert_packed_equal(p, ref, 4)
+
+
+def test_api_validates_caller_buffers(A):
+    """caller-supplied buffers are checked (device, contiguity,
+    dtype, size) before their pointers reach the C ABI."""
+    x = torch.randn(4, 1024, device=DEV)
+    p = A.compress(x, seed=1, bits=2)
+    with pytest.raises(A.ActnnError):
+        A.dequantize(p, out=torch.empty(4, 1000, device=DEV))            # too small
+    with pytest.raises(A.ActnnError):
+        A.dequantize(p, out=torch.empty(4, 2048, device=DEV)[:, ::2])    # strided
+    with pytest.raises(A.ActnnError):
+        A.dequantize(p, out=torch.empty(4, 1024, dtype=torch.float16, device=DEV))
+    bits, off = A.uniform_bits(4, 1024, 2, DEV)
+    with pytest.raises(A.ActnnError):
+        A.quantize(x, bits, off.to(torch.int32), 1)
+    with pytest.raises(A.ActnnError):
+        A.quantize(x, bits[:3], off, 1)
+    gmin, gmax, _ = A.group_stats(x)
+    with pytest.raises(A.ActnnError):
+        A.quantize(x, bits, off, 1, gmin, None)
+    with pytest.raises(A.ActnnError):
+        A.quantize(x, bits, off, 1, gmin[:-1], gmax)
+    S = torch.ones(8, dtype=torch.float64, device=DEV)
+    with pytest.raises(A.ActnnError):
+        A.allocate_bits(S, 16, 1024, gscale=torch.ones(8, device=DEV))   # fp32 gscale
+    with pytest.raises(A.ActnnError):
+        A.gradmag_gather(torch.ones(10, dtype=torch.float64, device=DEV),
+                         torch.zeros(3, dtype=torch.int32, device=DEV))
+    mask, _ = A.relu_pack(x)
+    with pytest.raises(A.ActnnError):
+        A.relu_backward(mask[:10], x)
+    x4 = torch.randn(2, 3, 16, 16, device=DEV)
+    y, idx = A.maxpool2d(x4, 3, 2, 1)
+    with pytest.raises(A.ActnnError):
+        A.maxpool2d_backward(idx, y[..., :-1].contiguous(), 16, 16, 3, 2, 1)
+    with pytest.raises(A.ActnnError):
+        A.maxpool2d_backward(idx.to(torch.int32), y, 16, 16, 3, 2, 1)
+    # the checks reject nothing valid
+    out = A.dequantize(p, out=torch.empty(4, 1024, device=DEV))
+    assert A.maxpool2d_backward(idx, y, 16, 16, 3, 2, 1).shape == x4.shape
+    assert p.nbytes() < p.capacity_bytes()
+    assert p.payload_bytes() == 4 * 4 * 32 * 2

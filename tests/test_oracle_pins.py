@@ -220,6 +220,55 @@ def test_degenerate_and_tiny_ranges():
     assert codes.max() == 0 and z == 0.0 and s == np.float32(2.0 ** -100) / np.float32(255)
 
 
+def test_nondegenerate_tiny_ranges():
+    """Tiny but non-degenerate ranges (SURVEY §8(d): R in {2^-100, 2^-90};
+    DESIGN reading 16 puts the threshold at 2^-96), where inv14 = RN(B/R) 2^14
+    reaches ~B 2^110 and members may be subnormal.
+    (1) Grid round trip: values k 2^-97, R = 3 2^-97 > 2^-96, b = 2 ->
+        codes = k and h_hat = h exactly.
+    (2) The threshold itself: R = 2^-96 quantises (non-zero codes), the float
+        just below it is degenerate (all codes 0, h_hat = Z).
+    (3) Unbiasedness for a group spanning [0, 2^-95] with subnormal
+        and zero members: Monte Carlo mean within 4 SE + 2^-14 scale."""
+    k = np.arange(256) % 4
+    h = (k * np.float32(2.0 ** -97)).astype(np.float32)
+    h[0], h[1] = 0.0, np.float32(3 * 2.0 ** -97)
+    seg, z, s = O.quantize_group(h, 2, 11, 0)
+    codes, out = O.dequantize_group(seg, 256, 2, z, s)
+    k[0], k[1] = 0, 3
+    assert np.array_equal(codes, k) and np.array_equal(out, h)
+
+    rng = np.random.default_rng(5)
+    for R, degenerate in ((np.float32(2.0 ** -96), False),
+                          (np.nextafter(np.float32(2.0 ** -96), np.float32(0)), True)):
+        g = (rng.random(256) * float(R)).astype(np.float32)
+        g[0], g[1] = 0.0, R
+        seg, z, s = O.quantize_group(g, 4, 3, 0)
+        codes, out = O.dequantize_group(seg, 256, 4, z, s)
+        if degenerate:
+            assert codes.max() == 0 and np.all(out == 0.0)
+        else:
+            assert codes.max() == 15 and np.count_nonzero(codes) > 200
+            assert np.all(np.abs(out.astype(np.float64) - g) <= float(s))
+
+    g = (rng.random(256) * 2.0 ** -95).astype(np.float32)
+    g[2::3] = (rng.random(85) * 2.0 ** -126).astype(np.float32)   # subnormal members
+    g[4::7] = 0.0
+    g[0], g[1] = 0.0, np.float32(2.0 ** -95)
+    assert np.count_nonzero((g > 0) & (g < 2.0 ** -126)) > 50
+    b, S = 2, 3000
+    acc = np.zeros(256)
+    for seed in range(S):
+        seg, z, s = O.quantize_group(g, b, seed, 3 * 256)
+        _, out = O.dequantize_group(seg, 256, b, z, s)
+        acc += out.astype(np.float64)
+    scale = float(s)
+    u = g.astype(np.float64) / scale
+    p = u - np.floor(u)
+    se = np.sqrt(np.maximum(p * (1 - p), 1e-30) / S) * scale
+    assert np.all(np.abs(acc / S - g) <= 4 * se + scale * 2.0 ** -14)
+
+
 def test_signed_zero_canonical():
     """DESIGN reading 17: Z is canonical +0 whether the group's zeros are +0 or -0."""
     h = np.zeros(256, np.float32)

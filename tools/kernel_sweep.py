@@ -1,5 +1,5 @@
 """Times K1/K3/K4 on a few C3 tensors (CUDA events, median of 10) for the
-library in ACTNN_LIB_VARIANT (or the default build).  Diagnostics only."""
+library loaded by tools/with_variant.py (or the default build).  Diagnostics only."""
 import ctypes
 import json
 import os
