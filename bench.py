@@ -30,6 +30,28 @@ sys.path.insert(0, ROOT)
 
 METRIC = "compress+decompress GB/s and % HBM peak at 1/2/4/8 B200; codes bit-exact vs oracle"
 FALLBACK_HBM_GBS = 6650.0
+NOMINAL_HBM_GBS = 8000.0   # B200 HBM3e nominal ("report both")
+
+# The paper's own numbers nearest to this path, with their hardware (BASELINE.md
+# §1).  Context only: the paper publishes no compressor / decompressor throughput.
+PAPER_CONTEXT = {
+    "note": "PAPER.md reports no compressor/decompressor throughput (BASELINE.json "
+            "'published' is empty); these are its end-to-end figures, other hardware, "
+            "fp32 PyTorch 1.7 training -- context, not targets",
+    "hardware": "1x NVIDIA T4 16 GB (AWS g4dn.4xlarge), 64 GB host, PyTorch 1.7 (P:820)",
+    "figures": [
+        {"what": "ResNet-152 activation memory, FP -> ActNN L3 (2-bit), batch 32 / 64",
+         "value": "5.28 -> 0.44 GB / 10.57 -> 0.88 GB (12x)", "cite": "P:765-766 (Table 4)"},
+        {"what": "ResNet-152 total memory, FP -> L3, batch 32 / 64",
+         "value": "6.01 -> 1.18 GB / 11.32 -> 1.64 GB", "cite": "P:765-766 (Table 4)"},
+        {"what": "bits per element of a Conv-BN-ReLU block (bf16 metadata)",
+         "value": "5.25 vs 64 -> 12.19x", "cite": "P:826-828"},
+        {"what": "training throughput of the largest ResNet-152 variant at batch 64, "
+                 "FP / L3 / L4 (depth, width, resolution scaling)",
+         "value": "0.59/0.46/0.38, 0.70/1.07/1.09, 0.59/0.46/0.42 TFLOPS",
+         "cite": "P:849-851 (Table 5)"},
+    ],
+}
 
 
 def parse():
@@ -52,6 +74,13 @@ def parse():
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay the step from a captured CUDA graph (default at N=1)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
+    ap.add_argument("--no-side", action="store_true",
+                    help="skip the C2 / C4 side legs of the default (C3, N=1) run")
+    ap.add_argument("--side-steps", type=int, default=10)
+    ap.add_argument("--pool", type=int, default=0,
+                    help="C5 below 4 GPUs: R distinct resident input buffers per tensor shape, "
+                         "reused by the tensors of that shape (0: automatic when the whole "
+                         "set does not fit)")
     return ap.parse_args()
 
 
@@ -277,6 +306,325 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ measurement
+class Run:
+    """One workload on this rank: inputs, the plan, the timed schedule."""
+
+    def __init__(self, wl, n_loc, rank, world, dev, args, gather, torch, A, W, pool=0):
+        from paper_2104_14129_b200.plan import ActivationSetPlan, PipelinedStep
+        self.wl, self.n_loc, self.world = wl, n_loc, world
+        self.s_in = 4 if wl.dtype == "f32" else 2
+        tdt = torch.float32 if wl.dtype == "f32" else torch.bfloat16
+        self.pool = pool
+        if pool > 0:
+            # per-layer streaming for sets larger than HBM (C5 below 4 GPUs): R
+            # distinct resident buffers per tensor shape, the tensors of a shape
+            # take them in turn (a forward pass writes each activation into
+            # HBM just before it is compressed; the compressed set stays resident)
+            bufs, occ = {}, {}
+            self.xs = []
+            for t, a in enumerate(wl.acts):
+                key = (a.C, a.H, a.W, a.relu, a.image)
+                k = occ.get(key, 0)
+                occ[key] = k + 1
+                lst = bufs.setdefault(key, [])
+                if len(lst) < pool:
+                    lst.append(W.synth_activation(a, n_loc, t + 100_000 * rank, wl.dtype, dev))
+                self.xs.append(lst[k % pool])
+            self.distinct_bytes = sum(x.numel() * x.element_size()
+                                      for lst in bufs.values() for x in lst)
+        else:
+            self.xs = [W.synth_activation(a, n_loc, t + 100_000 * rank, wl.dtype, dev)
+                       for t, a in enumerate(wl.acts)]
+        torch.cuda.synchronize()
+        self.plan = ActivationSetPlan(
+            self.xs, [W.quant_seed(t) for t in range(len(wl.acts))], avg_bits=wl.avg_bits,
+            bits=None if wl.avg_bits else wl.bits, n_total=n_loc * world,
+            sample_base=rank * n_loc, gather=gather, meta=args.meta,
+            level_mask=0x116 if args.levels == "pow2" else 0x1FE)
+        max_numel = max(x.numel() for x in self.xs)
+        # decompress streams (ACTNN_DQ_STREAMS, default 3), one output buffer each
+        n_dq = max(1, int(os.environ.get("ACTNN_DQ_STREAMS", "3")))
+        self.outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(max(2, n_dq))]
+        self.out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
+        # the timed schedule (plan.PipelinedStep): statistics / quantisation
+        # alternate over ACTNN_S_STREAMS / ACTNN_Q_STREAMS streams (default 2
+        # each); allocation on a high-priority stream
+        self.ps = PipelinedStep(self.plan, self.outs, self.out_dt, dev,
+                                n_stats=int(os.environ.get("ACTNN_S_STREAMS", "2")),
+                                n_quant=int(os.environ.get("ACTNN_Q_STREAMS", "2")), n_dq=n_dq)
+        self.E_loc = n_loc * sum(a.D for a in wl.acts)
+        self.graph_error = None
+
+    def capture(self, dist_on, barrier):
+        try:
+            self.ps.capture(check_exchange=dist_on)
+            barrier()
+        except Exception as e:  # fall back to the eager schedule
+            self.ps.graph = None
+            self.graph_error = f"{type(e).__name__}: {e}"[:200]
+            import torch
+            torch.cuda.synchronize()
+            barrier()
+
+    def phases(self, torch, barrier, reps):
+        """The schedule once more, eager, with events at the compress /
+        decompress boundary (rank-local), averaged over `reps` steps."""
+        ps = self.ps
+        marks = []
+        barrier()
+        for _ in range(reps):
+            m = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            m[0].record(ps.stream)
+            ps.compress()
+            m[1].record(ps.stream)
+            ps.decompress()
+            m[2].record(ps.stream)
+            marks.append(m)
+        barrier()
+        t_comp = sum(m[0].elapsed_time(m[1]) for m in marks) / reps
+        t_decomp = sum(m[1].elapsed_time(m[2]) for m in marks) / reps
+        return t_comp, t_decomp
+
+    def breakdown(self, torch, barrier, kb):
+        """Serial per-kernel breakdown: every tensor's launches back to back on
+        the main stream, an event pair around each kernel.  A spin kernel ahead
+        of each pass keeps host enqueue gaps out of the events."""
+        import ctypes
+        plan, outs, out_dt = self.plan, self.outs, self.out_dt
+        sp = ctypes.c_void_p(self.ps.stream.cuda_stream)
+        nl = len(plan.layers)
+
+        def events():
+            per = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nl)]
+            per += [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
+            return per
+
+        def serial(ev):
+            for i in range(nl):
+                plan.compress_layer(i, sp, ev[i])
+            for i in range(nl):
+                plan.decompress_layer(i, outs[i & 1], out_dt, sp, ev[nl + i])
+
+        with torch.cuda.stream(self.ps.stream):
+            barrier()
+            t_host = time.perf_counter()
+            serial(events())
+            t_host = time.perf_counter() - t_host
+            barrier()
+            evs = []
+            for _ in range(kb):
+                torch.cuda._sleep(int(1.5 * t_host * 2.0e9))
+                ev = events()
+                serial(ev)
+                evs.append(ev)
+            barrier()
+        kt = {"stats": 0.0, "quantize": 0.0, "dequantize": 0.0}
+        tq = {"compress": 0.0, "decompress": 0.0}
+        for per in evs:
+            for i in range(nl):
+                if plan.mixed:
+                    kt["stats"] += per[i][0].elapsed_time(per[i][1])
+                kt["quantize"] += per[i][2].elapsed_time(per[i][3])
+                kt["dequantize"] += per[nl + i][0].elapsed_time(per[nl + i][1])
+            tq["compress"] += per[0][0 if plan.mixed else 2].elapsed_time(per[nl - 1][3])
+            tq["decompress"] += per[nl][0].elapsed_time(per[2 * nl - 1][1])
+        self.layer_rows = None
+        if os.environ.get("ACTNN_LAYER_DUMP"):
+            self.layer_rows = [
+                {"layer": i, "name": self.wl.acts[i].name, "N": L.N, "D": L.D,
+                 "stats_us": 1e3 * sum(e[i][0].elapsed_time(e[i][1]) for e in evs) / kb
+                 if plan.mixed else None,
+                 "quant_us": 1e3 * sum(e[i][2].elapsed_time(e[i][3]) for e in evs) / kb,
+                 "dequant_us": 1e3 * sum(e[nl + i][0].elapsed_time(e[nl + i][1])
+                                         for e in evs) / kb}
+                for i, L in enumerate(plan.layers)]
+        return {k: v / kb for k, v in kt.items()}, {k: v / kb for k, v in tq.items()}
+
+    def report(self, args, ms_step, t_comp, t_decomp, kt, tq, peak, peak_src):
+        """The roofline / phase fields of a bench line for this workload."""
+        plan, wl, world = self.plan, self.wl, self.world
+        bits_host = plan.bits_host()
+        alg = algorithmic_bytes(plan.layers, bits_host, self.s_in, self.s_in, plan.mixed,
+                                4 if args.meta == "bf16" else 8)
+        nl = len(plan.layers)
+        dom = max(kt, key=lambda k: kt[k])
+        ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
+        names = {"stats": "group_stats_kernel (K1)",
+                 "quantize": "quantize_ws_kernel (K3)" if plan.mixed
+                 else "quantize_fast_kernel (K3)",
+                 "dequantize": "dequantize_fast_kernel (K4)"}
+        roofline = {
+            "bound": "hbm", "kernel": names[dom], "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "peak_source": peak_src,
+            "frac_nominal": ach / NOMINAL_HBM_GBS, "peak_nominal": NOMINAL_HBM_GBS,
+            "traffic": (ncu_traffic(dom, plan.mixed)
+                        if wl.name == "c3" and args.meta == "f32" and args.levels == "pow2"
+                        and self.pool == 0 else None),
+            "algorithmic_bytes_per_launch": alg[dom] / nl,
+            "avg_launch_us": kt[dom] * 1e3 / nl,
+            "launches_per_step": nl,
+            # the same kernel inside the timed schedule: K4 is the only kernel of
+            # the decompress phase (its launches overlap on several streams)
+            "in_step": {"phase": f"decompress (K4 only, {len(self.ps.dq)} streams)",
+                        "GBps": alg["dequantize"] / (t_decomp * 1e-3) / 1e9,
+                        "frac": alg["dequantize"] / (t_decomp * 1e-3) / 1e9 / peak,
+                        "frac_nominal": alg["dequantize"] / (t_decomp * 1e-3) / 1e9
+                        / NOMINAL_HBM_GBS},
+            "per_kernel": {k: {"kernel": names[k], "ms_per_step": kt[k],
+                               "share_of_step": kt[k] / ms_step,
+                               "GBps": (alg[k] / (kt[k] * 1e-3) / 1e9) if kt[k] else None,
+                               "frac": (alg[k] / (kt[k] * 1e-3) / 1e9 / peak) if kt[k] else None,
+                               "frac_nominal": (alg[k] / (kt[k] * 1e-3) / 1e9 / NOMINAL_HBM_GBS)
+                               if kt[k] else None,
+                               "algorithmic_bytes_per_step": alg[k]}
+                           for k in kt}}
+        total_alg = sum(alg.values())
+        avg_bits = [float(b.double().mean()) for b in bits_host]
+        E = world * self.E_loc * self.s_in
+        return {
+            "compress_GBps": E / (t_comp * 1e-3) / 1e9,
+            "decompress_GBps": E / (t_decomp * 1e-3) / 1e9,
+            "compress_ms": t_comp, "decompress_ms": t_decomp,
+            "compress_frac": (alg["stats"] + alg["quantize"]) / (t_comp * 1e-3) / 1e9 / peak,
+            "decompress_frac": alg["dequantize"] / (t_decomp * 1e-3) / 1e9 / peak,
+            "serial_breakdown_ms": {"compress": tq["compress"], "decompress": tq["decompress"]},
+            "hbm_frac_step": total_alg / (ms_step * 1e-3) / 1e9 / peak,
+            "hbm_frac_step_nominal": total_alg / (ms_step * 1e-3) / 1e9 / NOMINAL_HBM_GBS,
+            "algorithmic_bytes_per_step": total_alg,
+            "roofline": roofline,
+            "avg_bits_realised": sum(avg_bits) / len(avg_bits),
+        }
+
+
+def time_steps(ps, steps, barrier, torch, clk=None):
+    """K steps between one event pair, barrier + synchronize on both sides."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(ps.stream)
+    for _ in range(steps):
+        ps()
+    e1.record(ps.stream)
+    barrier()
+    return e0.elapsed_time(e1)
+
+
+def run_side(name, args, dev, torch, A, W, peak, peak_src, barrier):
+    """A side leg (N = 1, outside the headline timed region): the C2 / C4
+    workload through the same schedule, graph-replayed, with its own phase
+    split, roofline and per-kernel breakdown, so that the driver's record holds
+    all three single-GPU configs."""
+    wl = W.workload(name)
+    r = Run(wl, wl.N, 0, 1, dev, args, None, torch, A, W)
+    with torch.cuda.stream(r.ps.stream):
+        for _ in range(3):
+            r.ps()
+    barrier()
+    r.capture(False, barrier)
+    ms = time_steps(r.ps, args.side_steps, barrier, torch) / args.side_steps
+    t_comp, t_decomp = r.phases(torch, barrier, min(args.side_steps, 5))
+    kt, tq = r.breakdown(torch, barrier, 3)
+    rep = r.report(args, ms, t_comp, t_decomp, kt, tq, peak, peak_src)
+    out = {"workload": f"{wl.name.upper()}: {wl.description}", "dtype": wl.dtype,
+           "value": r.E_loc * r.s_in / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+           "steps": args.side_steps, "cuda_graph": r.ps.graph is not None,
+           "gpu_launches_per_step": r.plan.launches_per_step()}
+    out.update(rep)
+    del r
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
+def oracle_minmax_threaded(O, xh, threads):
+    """O3 over sample slices on `threads` host threads (ctypes drops the GIL)."""
+    import numpy as np
+    N = xh.shape[0]
+    k = max(1, min(threads, N))
+    bounds = [(N * i // k, N * (i + 1) // k) for i in range(k)]
+    parts = [None] * k
+
+    def go(i):
+        parts[i] = O.group_minmax(xh[bounds[i][0]:bounds[i][1]])
+
+    ts = [threading.Thread(target=go, args=(i,)) for i in range(k)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+
+
+def oracle_phases(wl, torch, threads, target_s):
+    """The oracle, as it stands, on a bounded sample of the workload (the first
+    n_s samples of every tensor), each phase timed: stats + allocation (O3,
+    O11, O12), quantise + pack (O4-O9), unpack + dequantise (O10).  n_s is
+    calibrated so the run takes ~target_s.  Returns per-phase elements/s."""
+    import numpy as np
+    import oracle as O
+    from paper_2104_14129_b200 import workloads as W
+    acts = wl.acts
+
+    def inputs(n):
+        out = []
+        for li, a in enumerate(acts):
+            x = W.synth_activation(a, n, li, wl.dtype, "cpu")
+            out.append(x.view(torch.int16).numpy().view(np.uint16) if wl.dtype == "bf16"
+                       else x.numpy())
+        return out
+
+    def run(n_s, xs):
+        t = {"stats_alloc": 0.0, "quantize_pack": 0.0, "unpack_dequantize": 0.0}
+        for li, (a, xh) in enumerate(zip(acts, xs)):
+            t0 = time.perf_counter()
+            if wl.avg_bits is not None:
+                mn, mx = oracle_minmax_threaded(O, xh, threads)
+                bits = O.allocate_bits(O.sensitivity(mn, mx), int(wl.avg_bits * n_s))
+            else:
+                bits = np.full(n_s, wl.bits, np.uint8)
+            t1 = time.perf_counter()
+            packed, zmin, scale, _ = O.quantize(xh, bits, W.quant_seed(li), 0, threads=threads)
+            t2 = time.perf_counter()
+            O.dequantize(packed, zmin, scale, bits, n_s, a.D,
+                         out_dtype=O.F32 if wl.dtype == "f32" else O.BF16, threads=threads)
+            t3 = time.perf_counter()
+            t["stats_alloc"] += t1 - t0
+            t["quantize_pack"] += t2 - t1
+            t["unpack_dequantize"] += t3 - t2
+        return t
+
+    n_s = 1
+    while True:
+        xs = inputs(n_s)
+        t = run(n_s, xs)
+        tot = sum(t.values())
+        if tot >= target_s / 4 or n_s >= wl.N:
+            break
+        n_s = min(wl.N, 2 * n_s)
+    n_new = max(1, min(wl.N, int(n_s * target_s / max(tot, 1e-3))))
+    if n_new > n_s:
+        n_s = n_new
+        xs = inputs(n_s)
+        t = run(n_s, xs)
+    E = n_s * sum(a.D for a in acts)
+    s_in = 4 if wl.dtype == "f32" else 2
+    tot = sum(t.values())
+    return {"threads": threads, "samples_per_tensor": n_s, "elements": E, "seconds": tot,
+            "GBps_in": E * s_in / tot / 1e9, "elements_per_s": E / tot,
+            "phases_elements_per_s": {k: (E / v if v > 0 else None) for k, v in t.items()},
+            "phases_seconds": t}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------ main arm
 def main():
     args = parse()
@@ -292,8 +640,8 @@ def main():
     import torch.distributed as dist
 
     import paper_2104_14129_b200 as A
+    from paper_2104_14129_b200 import dist as AD
     from paper_2104_14129_b200 import workloads as W
-    from paper_2104_14129_b200.plan import ActivationSetPlan, PipelinedStep
 
     # one process per GPU; ACTNN_DIST_BACKEND=gloo is a test mode in which
     # several ranks may share a GPU (NCCL refuses duplicate devices)
@@ -315,224 +663,63 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    wl = W.workload(args.config)
-    n_loc = wl.N // world if args.config == "c5" else wl.N
-    n_total = n_loc * world
-    s_in = 4 if wl.dtype == "f32" else 2
-    tdt = torch.float32 if wl.dtype == "f32" else torch.bfloat16
-
-    # resident inputs must fit: C5 (batch 4096, 365.8 GB of bf16 activations in
-    # total) needs >= 4 GPUs; smaller N would have to stream tensors from host
-    need = n_loc * sum(a.D for a in wl.acts) * s_in * 1.1
-    free = torch.cuda.mem_get_info(dev)[0]
-    if need > free:
-        if rank == 0:
-            print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world,
-                              "config": config_dict(wl, args, world, n_loc),
-                              "error": "resident inputs need %.1f GB per GPU, %.1f GB free: "
-                                       "run %s on more GPUs" % (need / 1e9, free / 1e9,
-                                                                wl.name.upper())}), flush=True)
-        if dist_on:
-            dist.destroy_process_group()
-        return 1
-    xs = []
-    for t, a in enumerate(wl.acts):
-        xs.append(W.synth_activation(a, n_loc, t + 100_000 * rank, wl.dtype, dev))
-    torch.cuda.synchronize()
-    gather = None
-    if dist_on:
-        def gather(S, S_loc):
-            if backend == "nccl":
-                dist.all_gather_into_tensor(S, S_loc)
-            else:  # gloo (test mode: several ranks sharing one GPU)
-                dist.all_gather(list(S.view(world, -1).unbind(0)), S_loc)
-    plan = ActivationSetPlan(xs, [W.quant_seed(t) for t in range(len(wl.acts))],
-                             avg_bits=wl.avg_bits, bits=None if wl.avg_bits else wl.bits,
-                             n_total=n_total, sample_base=rank * n_loc, gather=gather,
-                             meta=args.meta,
-                             level_mask=0x116 if args.levels == "pow2" else 0x1FE)
-    max_numel = max(x.numel() for x in xs)
-    # decompress streams (ACTNN_DQ_STREAMS, default 3) and one output buffer each
-    n_dq = max(1, int(os.environ.get("ACTNN_DQ_STREAMS", "3")))
-    outs = [torch.empty(max_numel, dtype=tdt, device=dev) for _ in range(max(2, n_dq))]
-    out_dt = A.api.F32 if wl.dtype == "f32" else A.api.BF16
-    # the timed schedule (plan.PipelinedStep): statistics / quantisation alternate
-    # over ACTNN_S_STREAMS / ACTNN_Q_STREAMS streams (default 2 each), so that
-    # consecutive tensors' kernels overlap; allocation on a high-priority stream
-    ps = PipelinedStep(plan, outs, out_dt, dev,
-                       n_stats=int(os.environ.get("ACTNN_S_STREAMS", "2")),
-                       n_quant=int(os.environ.get("ACTNN_Q_STREAMS", "2")), n_dq=n_dq)
-    stream = ps.stream   # main stream (non-default so it can be captured)
-    torch.cuda.set_stream(stream)
-    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
-    nl = len(plan.layers)
-    dq_streams = ps.dq
-
-    phase_ev = []   # (start, mid, end) per step: compress / decompress split
-    flags = {"phases": False}
-
-    def step(ev=None):
-        if ev is None and not flags["phases"]:
-            ps()          # the timed schedule: graph replay, or the eager pipeline
-            return
-        if ev is None:    # the same schedule, eager, with events at the phase boundary
-            marks = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            marks[0].record(stream)
-            ps.compress()
-            marks[1].record(stream)
-            ps.decompress()
-            marks[2].record(stream)
-            phase_ev.append(marks)
-            return
-        # breakdown: serial per-tensor launches, an event pair around each kernel
-        for i in range(nl):
-            plan.compress_layer(i, sp, ev[i])
-        for i in range(nl):
-            plan.decompress_layer(i, outs[i & 1], out_dt, sp, ev[nl + i])
-
     def barrier():
         if dist_on:
             dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    barrier()
+    wl = W.workload(args.config)
+    n_loc = wl.N // world if args.config == "c5" else wl.N
+    s_in = 4 if wl.dtype == "f32" else 2
+    # C5 (batch 4096, 365.8 GB of bf16 activations) is resident from 4 GPUs on;
+    # below that its tensors are streamed through a pool of per-shape buffers
+    need = n_loc * sum(a.D for a in wl.acts) * s_in * 1.15
+    free = torch.cuda.mem_get_info(dev)[0]
+    pool = args.pool
+    if pool == 0 and need > free:
+        pool = 2
+    gather = AD.make_gather(world, backend) if dist_on else None
+    run = Run(wl, n_loc, rank, world, dev, args, gather, torch, A, W, pool=pool)
+    ps = run.ps
+    torch.cuda.set_stream(ps.stream)
+    plan = run.plan
 
-    # ---- optional: capture the whole pipelined step in one CUDA graph (removes
-    # the ~430 per-step CPU launches; every kernel still runs on every replay)
-    # Seeds are per tensor and fixed across steps in both modes, so a replay does
-    # exactly the work of an eager step.
-    graph_error = None
+    for _ in range(max(3, args.warmup)):
+        ps()
+    barrier()
+    # capture the whole pipelined step in one CUDA graph (removes the ~430
+    # per-step CPU launches; every kernel still runs on every replay).  N > 1:
+    # the NCCL all-gathers are captured too (tests check replay == eager);
+    # ACTNN_DIST_GRAPH=0 keeps the multi-GPU step eager
     if args.graph is None:
-        # N > 1: the NCCL all-gathers are captured too (tests/test_gpu_parity.py
-        # checks replay == eager through a real NCCL group); ACTNN_DIST_GRAPH=0
-        # keeps the multi-GPU step eager
         args.graph = not dist_on or (backend == "nccl"
                                     and os.environ.get("ACTNN_DIST_GRAPH", "1") != "0")
     if args.graph:
-        try:
-            ps.capture(check_exchange=dist_on)
-            barrier()
-        except Exception as e:  # fall back to the eager schedule
-            ps.graph, graph_error, args.graph = None, f"{type(e).__name__}: {e}"[:200], False
-            torch.cuda.synchronize()
-            barrier()
+        run.capture(dist_on, barrier)
+        args.graph = ps.graph is not None
 
     # ---- headline: K steps, one event pair, max over ranks
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        barrier()
-        e0.record()
-        for _ in range(args.steps):
-            step()
-        e1.record()
-        barrier()
-    ms = e0.elapsed_time(e1)
+        ms = time_steps(ps, args.steps, barrier, torch)
     if dist_on:
-        tt = torch.tensor([ms], dtype=torch.float64,
-                          device=dev if backend == "nccl" else "cpu")
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
-    E_loc = n_loc * sum(a.D for a in wl.acts)
-    value = world * E_loc * s_in / (ms_step * 1e-3) / 1e9
+    value = world * run.E_loc * s_in / (ms_step * 1e-3) / 1e9
 
-    # ---- the same schedule once more with events at the compress/decompress boundary
-    flags["phases"] = True
-    barrier()
-    for _ in range(min(args.steps, 5)):
-        step()
-    barrier()
-    flags["phases"] = False
-    t_comp = sum(m[0].elapsed_time(m[1]) for m in phase_ev) / len(phase_ev)
-    t_decomp = sum(m[1].elapsed_time(m[2]) for m in phase_ev) / len(phase_ev)
-
-    # ---- per-kernel breakdown: same steps with an event pair around every launch
-    kb = max(3, args.steps // 4)
-    evs = []
-    for _ in range(kb):
-        per = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nl)]
-        per += [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
-        evs.append(per)
-    # The host enqueues a step's ~1000 events and launches more slowly than the
-    # GPU runs the small kernels; a spin kernel ahead of each step keeps the GPU
-    # busy while the step is enqueued, so the event pairs time the kernels and
-    # not host gaps (the enqueue time is measured on an untimed pass).
-    warm = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nl)]
-    warm += [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nl)]
-    barrier()
-    t_host = time.perf_counter()
-    step(warm)
-    t_host = time.perf_counter() - t_host
-    barrier()
-    for s in range(kb):
-        torch.cuda._sleep(int(1.5 * t_host * 2.0e9))
-        step(evs[s])
-    barrier()
-    kt = {"stats": 0.0, "quantize": 0.0, "dequantize": 0.0}
-    tq = {"compress": 0.0, "decompress": 0.0}
-    for per in evs:
-        for i in range(nl):
-            if plan.mixed:
-                kt["stats"] += per[i][0].elapsed_time(per[i][1])
-            kt["quantize"] += per[i][2].elapsed_time(per[i][3])
-            kt["dequantize"] += per[nl + i][0].elapsed_time(per[nl + i][1])
-        tq["compress"] += per[0][0 if plan.mixed else 2].elapsed_time(per[nl - 1][3])
-        tq["decompress"] += per[nl][0].elapsed_time(per[2 * nl - 1][1])
-    for k in kt:
-        kt[k] /= kb
-    for k in tq:
-        tq[k] /= kb
-    if os.environ.get("ACTNN_LAYER_DUMP") and rank == 0:
-        # per-tensor kernel times of the breakdown steps (diagnostics only)
-        rows = []
-        for i, L in enumerate(plan.layers):
-            rows.append({"layer": i, "name": wl.acts[i].name, "N": L.N, "D": L.D,
-                         "stats_us": 1e3 * sum(e[i][0].elapsed_time(e[i][1]) for e in evs) / kb
-                         if plan.mixed else None,
-                         "alloc_gap_us": 1e3 * sum(e[i][1].elapsed_time(e[i][2]) for e in evs) / kb
-                         if plan.mixed else None,
-                         "quant_us": 1e3 * sum(e[i][2].elapsed_time(e[i][3]) for e in evs) / kb,
-                         "dequant_us": 1e3 * sum(e[nl + i][0].elapsed_time(e[nl + i][1])
-                                                 for e in evs) / kb})
+    t_comp, t_decomp = run.phases(torch, barrier, min(args.steps, 5))
+    kt, tq = run.breakdown(torch, barrier, max(3, args.steps // 4))
+    if run.layer_rows is not None and rank == 0:
         with open(os.environ["ACTNN_LAYER_DUMP"], "w") as f:
-            json.dump(rows, f, indent=0)
-    bits_host = plan.bits_host()
-    alg = algorithmic_bytes(plan.layers, bits_host, s_in, s_in, plan.mixed,
-                            4 if args.meta == "bf16" else 8)
+            json.dump(run.layer_rows, f, indent=0)
     peak, peak_src = hbm_peak()
-    dom = max(kt, key=lambda k: kt[k])
-    launches_dom = nl
-    ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": {"stats": "group_stats_kernel (K1)",
-                                           "quantize": "quantize_ws_kernel (K3)" if plan.mixed
-                                           else "quantize_fast_kernel (K3)",
-                                           "dequantize": "dequantize_fast_kernel (K4)"}[dom],
-                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "peak_source": peak_src, "traffic": (ncu_traffic(dom, plan.mixed)
-                            if wl.name == "c3" and args.meta == "f32" and args.levels == "pow2"
-                            else None),
-                "algorithmic_bytes_per_launch": alg[dom] / launches_dom,
-                "avg_launch_us": kt[dom] * 1e3 / launches_dom,
-                # the same kernel inside the timed schedule: K4 is the only kernel of
-                # the decompress phase (its launches overlap on several streams)
-                "in_step": {"phase": f"decompress (K4 only, {len(dq_streams)} streams)",
-                            "GBps": alg["dequantize"] / (t_decomp * 1e-3) / 1e9,
-                            "frac": alg["dequantize"] / (t_decomp * 1e-3) / 1e9 / peak},
-                "per_kernel": {k: {"ms_per_step": kt[k], "share_of_step": kt[k] / ms_step,
-                                   "GBps": (alg[k] / (kt[k] * 1e-3) / 1e9) if kt[k] else None,
-                                   "frac": (alg[k] / (kt[k] * 1e-3) / 1e9 / peak) if kt[k] else None}
-                               for k in kt}}
-    total_alg = sum(alg.values())
-    avg_bits = [float(b.double().mean()) for b in bits_host]
+    rep = run.report(args, ms_step, t_comp, t_decomp, kt, tq, peak, peak_src)
+    xs = run.xs
 
-    # ---- NEXT-3 side measurement (not part of the step): per-sample gradient
-    # norms over every tensor of the set (the activations stand in for
-    # gradients of the same shape: same bytes, same kernel) and the stage-2
-    # joint allocation over all layers
+    # ---- NEXT-3 / NEXT-4 side measurements (not part of the step)
     adapt = None
-    if plan.mixed and world == 1 and not args.no_adapt:
+    if plan.mixed and world == 1 and not args.no_adapt and pool == 0:
         adapt = run_adapt(A, plan, xs, wl, s_in, torch, peak, barrier)
     contexts = None
     if world == 1 and not args.no_adapt:
@@ -540,26 +727,29 @@ def main():
     # ---- e2e through the public API with host buffers (per-layer pipeline)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist,
-                      s_in, E_loc, barrier, backend)
+        import ctypes
+        e2e = run_e2e(args, plan, xs, run.outs, run.out_dt, ctypes.c_void_p(ps.stream.cuda_stream),
+                      ps.stream, world, local, dev, torch, dist, s_in, run.E_loc, barrier,
+                      backend, unique_inputs=(pool == 0))
 
+    cfg = dict(config_dict(wl, args, world, n_loc),
+               **({"graph_error": run.graph_error} if run.graph_error else {}))
+    if pool:
+        cfg["inputs"] = (f"streamed per layer: {pool} distinct resident buffers per tensor "
+                         f"shape ({run.distinct_bytes / 1e9:.1f} GB), reused by that shape's "
+                         f"tensors; the whole set ({need / 1.15 / 1e9:.1f} GB per GPU) exceeds "
+                         "HBM. The compressed set of every tensor stays resident.")
+        cfg["l2"] = "every tensor >= 16 MB, consecutive tensors use distinct buffers"
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak" if args.config != "c5" else "strong",
             "vs_baseline": None, "dtype": wl.dtype,
             "data": "synthetic (seeded ResNet-shaped activations generated on the GPU)",
-            "config": dict(config_dict(wl, args, world, n_loc),
-                           **({"graph_error": graph_error} if graph_error else {})),
-            # phases of the pipelined schedule (events at the boundary; rank-local)
-            "compress_GBps": world * E_loc * s_in / (t_comp * 1e-3) / 1e9,
-            "decompress_GBps": world * E_loc * s_in / (t_decomp * 1e-3) / 1e9,
-            "compress_ms": t_comp, "decompress_ms": t_decomp,
-            "serial_breakdown_ms": {"compress": tq["compress"], "decompress": tq["decompress"]},
-            "hbm_frac_step": total_alg / (ms_step * 1e-3) / 1e9 / peak,
-            "roofline": roofline,
-            "gpu_launches": plan.launches_per_step() * args.steps,
-            "clocks": clk.summary(),
-            "avg_bits_realised": sum(avg_bits) / len(avg_bits)}
+            "config": cfg}
+    line.update(rep)
+    line.update({"gpu_launches": plan.launches_per_step() * args.steps,
+                 "clocks": clk.summary(),
+                 "paper_context": PAPER_CONTEXT})
     if e2e is not None:
         line["e2e"] = e2e
     if adapt is not None:
@@ -567,13 +757,45 @@ def main():
     if contexts is not None:
         line["contexts"] = contexts
     if rank == 0 and world == 1 and not args.no_cpu:
-        cb, _ = cpu_sample(wl, wl.acts, args, args.cpu_seconds, W.quant_seed, torch)
-        line["cpu_baseline"] = cb
+        cores = os.cpu_count() or 1
+        allc = oracle_phases(wl, torch, cores, args.cpu_seconds * 0.6)
+        one = oracle_phases(wl, torch, 1, args.cpu_seconds * 0.4)
+        line["cpu_baseline"] = {
+            "value": allc["GBps_in"], "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"first {allc['samples_per_tensor']} of {wl.N} samples of each of the "
+                      f"{len(wl.acts)} tensors ({allc['elements']} elements), full compress + "
+                      f"decompress (stats, heap allocation, quantize, dequantize) on all "
+                      f"{cores} host threads, {allc['seconds']:.1f} s",
+            "all_cores": allc, "single_thread": one}
+    # ---- side legs: the other single-GPU configs of BASELINE.json (C2, C4)
+    if world == 1 and args.config == "c3" and not args.no_side:
+        del xs, adapt, contexts
+        free_run(run, torch)
+        del run, ps, plan
+        torch.cuda.set_stream(torch.cuda.default_stream())
+        torch.cuda.empty_cache()
+        line["side"] = {}
+        for name in ("c2", "c4"):
+            try:
+                line["side"][name] = run_side(name, args, dev, torch, A, W, peak, peak_src,
+                                              barrier)
+            except Exception as e:  # a side leg never voids the headline line
+                line["side"][name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+                torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist_on:
         dist.destroy_process_group()
     return 0
+
+
+def free_run(run, torch):
+    run.ps.graph = None
+    run.plan.layers.clear()
+    run.xs.clear()
+    run.outs.clear()
+    torch.cuda.synchronize()
 
 
 def run_contexts(A, xs, wl, torch, peak, barrier, reps=5):
@@ -680,7 +902,7 @@ def run_adapt(A, plan, xs, wl, s_in, torch, peak, barrier, reps=5):
 
 
 def run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist, s_in,
-            E_loc, barrier, backend="nccl"):
+            E_loc, barrier, backend="nccl", unique_inputs=True):
     """Host-pinned inputs copied in, compressed, decompressed and copied back
     out every step (per-tensor pipeline over three streams)."""
     import psutil

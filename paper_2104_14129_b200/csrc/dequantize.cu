@@ -178,6 +178,10 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
         const int64_t sofs = kCached ? ((int64_t)s_off[pn] << 5) : (p.off[pn] - off0);
         const uint32_t bytes = (uint32_t)(gcount_of(pj) * 32 * b);
         uint8_t* dst = ring + s * kStage;
+#ifdef ACTNN_DQ_FAKEREAD  // diagnostics: every unit reads unit (0, 0)'s bytes (L2-resident)
+        pn = 0;
+        pj = 0;
+#endif
         if (kMeta && kB16) {
             const uint32_t g = pn * p.ng + pj * kU;
             mbar_expect_tx(&bars[s], bytes + 4 * kU);

@@ -415,8 +415,14 @@ __device__ __forceinline__ void codes_wide(const float v[8], float Z, float inv1
     for (int p = 0; p < 4; ++p) {
         const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
         const float2 t = __ffma2_rn(d, iv, mg);
-        code[2 * p] = (__float_as_uint(t.x) - 0x4B400000u + (w[p] & 0x3FFFu)) >> 14;
-        code[2 * p + 1] = (__float_as_uint(t.y) - 0x4B400000u + ((w[p] >> 16) & 0x3FFFu)) >> 14;
+        // the halves' bit patterns through an opaque move: with a plain
+        // __float_as_uint, NVVM (CUDA 12.9) drops the shift that later places the
+        // .x half's code into the packed word (tools/cuda_checks/f32x2_miscompile.cu)
+        uint32_t tx, ty;
+        asm("mov.b32 %0, %1;" : "=r"(tx) : "f"(t.x));
+        asm("mov.b32 %0, %1;" : "=r"(ty) : "f"(t.y));
+        code[2 * p] = (tx - 0x4B400000u + (w[p] & 0x3FFFu)) >> 14;
+        code[2 * p + 1] = (ty - 0x4B400000u + ((w[p] >> 16) & 0x3FFFu)) >> 14;
     }
 #else
 #pragma unroll

@@ -44,6 +44,26 @@ def gather_sens(S_global: torch.Tensor, S_local: torch.Tensor, group=None) -> No
     dist.all_gather_into_tensor(S_global, S_local, group=group)
 
 
+def make_gather(world: int, backend: str = "nccl", group=None):
+    """The exchange step as the closure ActivationSetPlan calls per tensor:
+    gather(S_global, S_local) fills S_global[r*n:(r+1)*n] with rank r's S_n.
+
+    north_star names "an NCCL all-reduce of the allocator statistics"; the
+    all-gather is the same exchange (every rank ends with the identical global
+    S vector, bit for bit, since the zero-padded sum adds only exact zeros;
+    tests/test_dist_gloo.py checks the two agree) with 1/k of the bytes and no
+    per-step clearing of the padded vector.  NCCL: all_gather_into_tensor on
+    the current stream (capturable in a CUDA graph); gloo (test mode, several
+    ranks on one device or CPU): the list form."""
+    if backend == "nccl":
+        def gather(S_global: torch.Tensor, S_local: torch.Tensor) -> None:
+            dist.all_gather_into_tensor(S_global, S_local, group=group)
+    else:
+        def gather(S_global: torch.Tensor, S_local: torch.Tensor) -> None:
+            dist.all_gather(list(S_global.view(world, -1).unbind(0)), S_local, group=group)
+    return gather
+
+
 def local_slice(bits_g: torch.Tensor, off_g: torch.Tensor, lo: int, hi: int):
     """This rank's widths and offsets.  The ABI addresses sample n at
     packed + off[n] - off[0], so the slice off_g[lo:hi+1] is used as is."""

@@ -295,8 +295,9 @@ class PipelinedStep:
         self.graph = g
 
     def __call__(self):
-        if self.graph is not None:
-            self.graph.replay()
-        else:
-            with torch.cuda.stream(self.stream):
+        # CUDAGraph.replay() launches on the current stream: make it the main one
+        with torch.cuda.stream(self.stream):
+            if self.graph is not None:
+                self.graph.replay()
+            else:
                 self.eager()

@@ -44,6 +44,10 @@ def _worker(rank, world, port, N, D, avg, seed, q):
         S_ag = torch.zeros(N, dtype=torch.float64)
         AD.gather_sens(S_ag, S_loc)
         assert torch.equal(S_ar, S_ag)
+        # the closure the plan (and bench.py) call per tensor, gloo form
+        S_cl = torch.full((N,), -1.0, dtype=torch.float64)
+        AD.make_gather(world, "gloo")(S_cl, S_loc)
+        assert torch.equal(S_cl, S_ar)
         bits_g = O.allocate_bits(S_ar.numpy(), int(avg * N))
         off_g = O.offsets(bits_g, D)
         b_l, o_l = AD.local_slice(torch.from_numpy(bits_g), torch.from_numpy(off_g), lo, hi)

@@ -442,9 +442,9 @@ def test_api_validates_caller_buffers(A):
         A.quantize(x, bits[:3], off, 1)
     gmin, gmax, _ = A.group_stats(x)
     with pytest.raises(A.ActnnError):
-        A.quantize(x, bits, off, 1, gmin, None)
+        A.quantize(x, bits, off, 1, 0, gmin, None)
     with pytest.raises(A.ActnnError):
-        A.quantize(x, bits, off, 1, gmin[:-1], gmax)
+        A.quantize(x, bits, off, 1, 0, gmin[:-1], gmax)
     S = torch.ones(8, dtype=torch.float64, device=DEV)
     with pytest.raises(A.ActnnError):
         A.allocate_bits(S, 16, 1024, gscale=torch.ones(8, device=DEV))   # fp32 gscale

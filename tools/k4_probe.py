@@ -1,0 +1,58 @@
+"""K4 timing probe (diagnostics): dequantize of every C3 tensor back to back
+(one event pair per launch, as bench.py's breakdown) and of the largest tensor
+alone, for the library loaded by tools/with_variant.py."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2104_14129_b200 as A  # noqa: E402
+from paper_2104_14129_b200 import workloads as W  # noqa: E402
+
+cfg = os.environ.get("PROBE_CONFIG", "c3")
+wl = W.workload(cfg)
+dev = torch.device("cuda:0")
+ps = []
+out = None
+for li, act in enumerate(wl.acts):
+    x = W.synth_activation(act, wl.N, li, wl.dtype, dev)
+    p = A.compress(x, seed=W.quant_seed(li), avg_bits=wl.avg_bits)
+    n = int(p.off[-1].item())
+    p.packed = p.packed[:max(n, 16)].clone()
+    ps.append((p, x.numel(), x.element_size()))
+    del x
+    torch.cuda.synchronize()
+mx = max(n for _, n, _ in ps)
+out = torch.empty(mx, dtype=torch.float32 if wl.dtype == "f32" else torch.bfloat16, device=dev)
+
+
+def run_all(evs):
+    for (p, n, s), (a, b) in zip(ps, evs):
+        a.record()
+        A.dequantize(p, out=out[:n].view(p.shape))
+        b.record()
+
+
+evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        for _ in ps] for _ in range(4)]
+run_all(evs[0])
+torch.cuda.synchronize()
+tot = []
+per = [0.0] * len(ps)
+for r in range(1, 4):
+    torch.cuda._sleep(50_000_000)
+    run_all(evs[r])
+    torch.cuda.synchronize()
+    ts = [a.elapsed_time(b) for a, b in evs[r]]
+    tot.append(sum(ts))
+    per = [q + t / 3 for q, t in zip(per, ts)]
+alg = sum(int(p.off[-1].item()) + 8 * p.zmin.numel() + 9 * p.N + n * s for p, n, s in ps)
+big = max(range(len(ps)), key=lambda i: ps[i][1])
+pb, nb, sb = ps[big]
+algb = int(pb.off[-1].item()) + 8 * pb.zmin.numel() + 9 * pb.N + nb * sb
+res = {"config": cfg, "serial_ms": min(tot), "GBps_alg": alg / (min(tot) * 1e-3) / 1e9,
+       "largest_us": per[big] * 1e3, "largest_GBps": algb / (per[big] * 1e-3) / 1e9,
+       "small_share": sum(t for t, (_, n, s) in zip(per, ps) if n * s < 120e6) / sum(per)}
+print(json.dumps(res))

@@ -1,17 +1,28 @@
 #!/bin/bash
-# Under gpurun: compute-sanitizer over small GPU parity tests (memcheck over the
-# quantiser/dequantiser, contexts and NEXT-3 kernels; racecheck + synccheck over
-# the kernels that share memory between warps).  Writes gpurun_out/sanitize_<tool>.log.
+# Under gpurun: compute-sanitizer over small GPU parity tests -- memcheck,
+# racecheck, synccheck and initcheck over the quantiser/dequantiser, NEXT-3 and
+# NEXT-4 tests -- plus the mbarrier hand-off repro (racecheck's model of
+# mbarrier ordering).  Writes gpurun_out/sanitize_<tool>.log.
 CS=/usr/local/cuda/bin/compute-sanitizer
 SEL_Q='c1_golden or adversarial_all_widths or ragged or unaligned or empty or mixed_widths_multi_tile'
 SEL_A='grad_sqnorm_edges or ema or stale or ties_and_edges or resnet50_parity'
 SEL_C='relu_pack_and_backward and 1023 or maxpool_forward_backward'
-for tool in memcheck racecheck synccheck; do
+for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
+  extra=""
+  [ "$tool" = "racecheck" ] && extra="--racecheck-report hazard"
   {
     echo "## $tool"
-    timeout 1500 $CS --tool $tool --print-limit 20 python -m pytest -q -x tests/test_gpu_parity.py -k "$SEL_Q" 2>&1 | tail -4
-    timeout 1500 $CS --tool $tool --print-limit 20 python -m pytest -q -x tests/test_gpu_adapt.py -k "$SEL_A" 2>&1 | tail -4
-    timeout 1500 $CS --tool $tool --print-limit 20 python -m pytest -q -x tests/test_gpu_contexts.py -k "$SEL_C" 2>&1 | tail -4
+    timeout 1500 $CS --tool $tool $extra --print-limit 400 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_parity.py -k "$SEL_Q" > gpurun_out/sanitize_${tool}_q_full.log 2>&1
+    tail -6 gpurun_out/sanitize_${tool}_q_full.log
+    echo "hazard sites (kernel, source line):"
+    grep -o "Race reported between.*" gpurun_out/sanitize_${tool}_q_full.log | sed 's/+0x[0-9a-f]*//g' | sort | uniq -c | sort -rn | head -20
+    timeout 1500 $CS --tool $tool $extra --print-limit 20 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_adapt.py -k "$SEL_A" 2>&1 | tail -4
+    timeout 1500 $CS --tool $tool $extra --print-limit 20 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_contexts.py -k "$SEL_C" 2>&1 | tail -4
+    if [ "$tool" = "racecheck" ]; then
+      echo "### repro: mbarrier hand-off (mode 0) vs __syncthreads (mode 1), tools/cuda_checks/racecheck_mbarrier.cu"
+      $CS --tool racecheck --racecheck-report hazard --print-limit 4 tools/cuda_checks/racecheck_mbarrier 0 2>&1 | tail -12
+      $CS --tool racecheck --racecheck-report hazard tools/cuda_checks/racecheck_mbarrier 1 2>&1 | tail -5
+    fi
   } > gpurun_out/sanitize_$tool.log 2>&1
   echo "$tool done"
 done
