@@ -9,7 +9,9 @@
 // Lane l reads the b bytes holding its 8 codes from shared memory (the (Z,
 // scale) pairs are broadcast reads) and writes its 8 consecutive outputs with
 // one 256-bit (fp32) or 128-bit (bf16) store, so each warp store covers whole
-// 32 B sectors.  (float)code uses the exact 2^23 magic; dequantisation is one
+// 32 B sectors -- or, for large fp32 outputs (kTS), into a per-warp staging
+// buffer in shared memory that one bulk copy (cp.async.bulk shared -> global)
+// writes out per unit.  (float)code uses the exact 2^23 magic; dequantisation is one
 // __ffma2_rn per element pair (single rounding, O10).
 #include "device.cuh"
 #include "launch.h"
@@ -33,8 +35,45 @@ constexpr int kS = ACTNN_DQ_S;            // stages per warp
 constexpr int kPay = kU * 32 * 8;         // payload bytes at the widest (b = 8)
 constexpr int kStage = kPay + 8 * kU;     // + kU zero points + kU scales
 constexpr int kNCap = 2048;
-constexpr size_t kSmem = (size_t)kWarps * kS * kStage + (size_t)kWarps * kS * 8 + kNCap +
-                         4 * (kNCap + 1);
+// TMA-store variant (kTS): each warp also owns kO output staging buffers of one
+// unit; the outputs go shared -> global by cp.async.bulk (SASS UBLKCP.S.G), so
+// the write stream leaves the SM through the TMA engine instead of the LSU.
+// ACTNN_DQ_TS: 0 never, 1 always, 2 (default) for fp32 outputs of at least
+// ACTNN_DQ_TS_MIN_MB megabytes -- measured per tensor size on the C3 / C4 sets
+// (tools/k4_probe.py): the TMA-store kernel (one CTA of 8 warps per SM, 4
+// staging buffers per warp) reaches 6.06 TB/s on the 822 MB C3 tensors against
+// 5.44 for the LSU-store kernel, is even at 205 MB and slower below (fewer
+// warps to cover the launch ramp) and on bf16 outputs.
+#ifndef ACTNN_DQ_TS
+#define ACTNN_DQ_TS 2
+#endif
+#ifndef ACTNN_DQ_TS_MIN_MB
+#define ACTNN_DQ_TS_MIN_MB 192
+#endif
+#ifndef ACTNN_DQ_O
+#define ACTNN_DQ_O 4
+#endif
+#ifndef ACTNN_DQ_TSW
+#define ACTNN_DQ_TSW 8
+#endif
+#ifndef ACTNN_DQ_TSMINB
+#define ACTNN_DQ_TSMINB 1
+#endif
+constexpr int kO = ACTNN_DQ_O;
+template <bool kTS>
+__host__ __device__ constexpr int warps() { return kTS ? ACTNN_DQ_TSW : kWarps; }
+template <bool kTS>
+__host__ __device__ constexpr size_t smem_base() {
+    return (size_t)warps<kTS>() * kS * kStage + (size_t)warps<kTS>() * kS * 8 + kNCap +
+           4 * (kNCap + 1);
+}
+template <bool kTS>
+__host__ __device__ constexpr size_t stg_off() { return (smem_base<kTS>() + 127) / 128 * 128; }
+template <typename TO, bool kTS>
+__host__ __device__ constexpr size_t smem_bytes() {
+    return kTS ? stg_off<kTS>() + (size_t)warps<kTS>() * kO * kU * kG * sizeof(TO)
+               : smem_base<kTS>();
+}
 
 struct DParams {
     const uint8_t* packed;
@@ -89,8 +128,54 @@ __device__ __forceinline__ uint32_t magic_code(uint64_t pay, int j) {
     }
 }
 
-// One group: the lane's 8 codes -> 8 outputs, one vector store.
-template <typename TO, int b>
+// Shared-memory staging stores of a lane's 8 outputs.  fp32: two 16-byte
+// halves, the lanes of each quarter warp alternating which half goes first so
+// that every st.shared.v4 covers all 32 banks once; bf16: one 16-byte store.
+__device__ __forceinline__ void sts8(float* p, const float v[8]) {
+    const int lane = threadIdx.x & 31;
+    const int h = (lane >> 2) & 1;
+    const uint32_t a = smem_u32(p);
+    const uint32_t a0 = a + 16 * h, a1 = a + 16 * (h ^ 1);
+    float f0[4], f1[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // selects, not a dynamically indexed (local) array
+        f0[i] = h ? v[4 + i] : v[i];
+        f1[i] = h ? v[i] : v[4 + i];
+    }
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a0), "f"(f0[0]), "f"(f0[1]),
+                 "f"(f0[2]), "f"(f0[3])
+                 : "memory");
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a1), "f"(f1[0]), "f"(f1[1]),
+                 "f"(f1[2]), "f"(f1[3])
+                 : "memory");
+}
+__device__ __forceinline__ void sts8(uint16_t* p, const float v[8]) {
+    const uint32_t a = pack_bf16x2(v[0], v[1]), b = pack_bf16x2(v[2], v[3]);
+    const uint32_t c = pack_bf16x2(v[4], v[5]), d = pack_bf16x2(v[6], v[7]);
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(a), "r"(b),
+                 "r"(c), "r"(d)
+                 : "memory");
+}
+
+// cp.async.bulk shared -> global (bulk async-group of the issuing thread)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// at most N of this thread's bulk groups still reading shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// One group: the lane's 8 codes -> 8 outputs, one vector store (kSh: into the
+// shared staging buffer instead of global memory).
+template <typename TO, int b, bool kSh = false>
 __device__ __forceinline__ void dequant_group(uint64_t pay, float Z, float s, TO* dst) {
     const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
     const float2 zz = make_float2(Z, Z), ss = make_float2(s, s);
@@ -104,50 +189,56 @@ __device__ __forceinline__ void dequant_group(uint64_t pay, float Z, float s, TO
         o[2 * p] = c.x;
         o[2 * p + 1] = c.y;
     }
-    store8(dst, o);
+    if constexpr (kSh)
+        sts8(dst, o);
+    else
+        store8(dst, o);
 }
 
 // A unit: zq/sq = the unit's 4 zero points / scales.
-template <typename TO, int b, bool kFullUnit>
+template <typename TO, int b, bool kFullUnit, bool kSh = false>
 __device__ __forceinline__ void dequant_unit(const uint8_t* st, int gcount, const float (&zq)[kU],
                                              const float (&sq)[kU], TO* dst, int lane) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
         if (kFullUnit || u < gcount) {
             const uint64_t pay = stage_payload<b>(st + u * 32 * b, lane);
-            dequant_group<TO, b>(pay, zq[u], sq[u], dst + u * kG + lane * 8);
+            dequant_group<TO, b, kSh>(pay, zq[u], sq[u], dst + u * kG + lane * 8);
         }
     }
 }
 
-template <typename TO, int b>
+template <typename TO, int b, bool kSh = false>
 __device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount,
                                                  const float (&zq)[kU], const float (&sq)[kU],
                                                  TO* dst, int lane) {
     if (gcount == kU)
-        dequant_unit<TO, b, true>(st, gcount, zq, sq, dst, lane);
+        dequant_unit<TO, b, true, kSh>(st, gcount, zq, sq, dst, lane);
     else
-        dequant_unit<TO, b, false>(st, gcount, zq, sq, dst, lane);
+        dequant_unit<TO, b, false, kSh>(st, gcount, zq, sq, dst, lane);
 }
 
 // kCached: (bits, off) of all samples in shared memory (N <= kNCap).
 // kMeta: the unit's metadata travels in the stage (ng % 4 == 0).
 // kB16: NEXT-1 bf16 metadata words (Z', R'): lane u < 4 widens group u's word
 // and computes scale = RN(R' / B) once, the unit's lanes get it by shuffle.
-template <typename TO, bool kCached, bool kMeta, bool kB16>
-__global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
+template <typename TO, bool kCached, bool kMeta, bool kB16, bool kTS>
+__global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACTNN_DQ_MINB)
     dequantize_fast_kernel(const __grid_constant__ DParams p) {
+    constexpr int kW = warps<kTS>();
     extern __shared__ __align__(128) uint8_t smem[];
+    TO* stg = reinterpret_cast<TO*>(smem + stg_off<kTS>()) + (size_t)(threadIdx.x >> 5) * kO * kU * kG;
+    uint32_t ounit = 0;  // units this warp has staged (kTS)
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     uint8_t* ring = smem + (size_t)w * kS * kStage;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kS * kStage) + w * kS;
-    uint8_t* s_bits = smem + (size_t)kWarps * kS * kStage + (size_t)kWarps * kS * 8;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kW * kS * kStage) + w * kS;
+    uint8_t* s_bits = smem + (size_t)kW * kS * kStage + (size_t)kW * kS * 8;
     uint32_t* s_off = reinterpret_cast<uint32_t*>(s_bits + kNCap);
 
     const int64_t off0 = p.off[0];
     if (kCached) {
-        for (uint32_t i = threadIdx.x; i < p.N; i += kBlock) {
+        for (uint32_t i = threadIdx.x; i < p.N; i += kW * 32) {
             s_bits[i] = p.bits[i];
             s_off[i] = (uint32_t)((p.off[i] - off0) >> 5);
         }
@@ -159,7 +250,7 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
     }
     __syncthreads();
 
-    const uint32_t gw = blockIdx.x * kWarps + w;
+    const uint32_t gw = blockIdx.x * kW + w;
     TO* __restrict__ out = static_cast<TO*>(p.out);
     auto advance = [&](uint32_t& n, uint32_t& j) {
         n += p.step_n;
@@ -269,29 +360,42 @@ __global__ void __launch_bounds__(kBlock, ACTNN_DQ_MINB)
                 }
             }
         }
-        if (b == 2) dequant_unit_any<TO, 2>(st, gcount, zq, sq, dst, lane);
-        else if (b == 1) dequant_unit_any<TO, 1>(st, gcount, zq, sq, dst, lane);
-        else if (b == 4) dequant_unit_any<TO, 4>(st, gcount, zq, sq, dst, lane);
-        else if (b == 8) dequant_unit_any<TO, 8>(st, gcount, zq, sq, dst, lane);
-        else if (b == 3) dequant_unit<TO, 3, false>(st, gcount, zq, sq, dst, lane);
-        else if (b == 5) dequant_unit<TO, 5, false>(st, gcount, zq, sq, dst, lane);
-        else if (b == 6) dequant_unit<TO, 6, false>(st, gcount, zq, sq, dst, lane);
-        else if (b == 7) dequant_unit<TO, 7, false>(st, gcount, zq, sq, dst, lane);
+        TO* ob = dst;
+        if constexpr (kTS) {
+            // staging buffer ounit % kO: its previous bulk store must have read it
+            ob = stg + (size_t)(ounit % kO) * (kU * kG);
+            if (lane == 0) bulk_wait_read<kO - 1>();
+            __syncwarp();
+        }
+        if (b == 2) dequant_unit_any<TO, 2, kTS>(st, gcount, zq, sq, ob, lane);
+        else if (b == 1) dequant_unit_any<TO, 1, kTS>(st, gcount, zq, sq, ob, lane);
+        else if (b == 4) dequant_unit_any<TO, 4, kTS>(st, gcount, zq, sq, ob, lane);
+        else if (b == 8) dequant_unit_any<TO, 8, kTS>(st, gcount, zq, sq, ob, lane);
+        else if (b == 3) dequant_unit<TO, 3, false, kTS>(st, gcount, zq, sq, ob, lane);
+        else if (b == 5) dequant_unit<TO, 5, false, kTS>(st, gcount, zq, sq, ob, lane);
+        else if (b == 6) dequant_unit<TO, 6, false, kTS>(st, gcount, zq, sq, ob, lane);
+        else if (b == 7) dequant_unit<TO, 7, false, kTS>(st, gcount, zq, sq, ob, lane);
         // the stage's shared loads were consumed by the stores above: re-arm it
         // (cross-proxy WAR: each lane's generic loads are ordered before the
         // async-proxy bulk write by fence.proxy.async, all lanes before lane 0's
-        // issue by the __syncwarp)
+        // issue by the __syncwarp).  kTS: the same fence orders the lanes'
+        // staging writes before the async-proxy bulk store that reads them.
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
+            if constexpr (kTS) bulk_s2g(dst, ob, (uint32_t)(gcount * kG * (int)sizeof(TO)));
             if (pn < p.N) issue(pn, pj, stage);
             advance(pn, pj);
         }
+        if constexpr (kTS) ++ounit;  // every lane: they all index the staging ring
         if (++stage == kS) {
             stage = 0;
             phase ^= 1u;
         }
         advance(n, j);
+    }
+    if constexpr (kTS) {
+        if (lane == 0) bulk_wait_all();  // shared memory stays valid until the stores read it
     }
 }
 
@@ -332,16 +436,29 @@ __global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(const __grid
     }
 }
 
-template <typename TO, bool kCached, bool kMeta, bool kB16>
-void launch_fast(const DParams& p0, int64_t units, cudaStream_t s) {
-    const void* k = (const void*)dequantize_fast_kernel<TO, kCached, kMeta, kB16>;
+template <typename TO, bool kCached, bool kMeta, bool kB16, bool kTS>
+void launch_fast_t(const DParams& p0, int64_t units, cudaStream_t s) {
+    constexpr size_t kSmem = smem_bytes<TO, kTS>();
+    const void* k = (const void*)dequantize_fast_kernel<TO, kCached, kMeta, kB16, kTS>;
     ensure_smem_attr(k, kSmem);  // opt-in above 48 KB of dynamic smem
     DParams p = p0;
-    const int grid = grid_for(k, kBlock, kSmem, (units + kWarps - 1) / kWarps);
-    const uint32_t nwarps = (uint32_t)grid * kWarps;
+    constexpr int kW = warps<kTS>();
+    const int grid = grid_for(k, kW * 32, kSmem, (units + kW - 1) / kW);
+    const uint32_t nwarps = (uint32_t)grid * kW;
     p.step_n = nwarps / p.nb;
     p.step_j = nwarps % p.nb;
-    dequantize_fast_kernel<TO, kCached, kMeta, kB16><<<grid, kBlock, kSmem, s>>>(p);
+    dequantize_fast_kernel<TO, kCached, kMeta, kB16, kTS><<<grid, kW * 32, kSmem, s>>>(p);
+}
+
+template <typename TO, bool kCached, bool kMeta, bool kB16>
+void launch_fast(const DParams& p, int64_t units, cudaStream_t s) {
+    const bool ts = ACTNN_DQ_TS == 1 ||
+                    (ACTNN_DQ_TS == 2 && sizeof(TO) == 4 &&
+                     (int64_t)p.N * p.D * (int64_t)sizeof(TO) >= (int64_t)ACTNN_DQ_TS_MIN_MB << 20);
+    if (ts)
+        launch_fast_t<TO, kCached, kMeta, kB16, true>(p, units, s);
+    else
+        launch_fast_t<TO, kCached, kMeta, kB16, false>(p, units, s);
 }
 
 template <typename TO>

@@ -278,3 +278,28 @@ def test_uncached_mixed_path_n4096_end_to_end(A, W):
     assert np.array_equal(host(p.packed[:int(off[-1])]), packed)
     assert np.array_equal(host(p.zmin).view(np.uint32), zmin.ravel().view(np.uint32))
     assert np.array_equal(out_bits(out.reshape(-1), out.numel()), oout.ravel())
+
+
+@pytest.mark.parametrize("N,D", [(4100, 256 * 49), (4100, 256 * 48), (2048, 256 * 100),
+                                 (2000, 256 * 101)])
+def test_tma_store_dequantize_large_fp32(A, W, N, D):
+    """fp32 outputs of >= 192 MB take the TMA-store K4 (shared-memory staging,
+    cp.async.bulk shared -> global): cached / uncached (bits, off) tables,
+    metadata staged (ng % 4 == 0) or read directly, ragged 4-group tails, all
+    widths; every dequantised value against the oracle."""
+    act = W.Act("t", D // 256, 16, 16, False)
+    x = W.synth_activation(act, N, 91, "f32", DEV)
+    assert x.numel() * 4 >= 192 << 20
+    cyc = np.array([2, 1, 4, 8, 3, 5, 6, 7, 1, 2], np.uint8)
+    bits_np = cyc[np.arange(N) % len(cyc)]
+    p = _run_large_n(A, x, bits_np, 5150, 3, two_pass=True)
+    out = A.dequantize(p, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    xh = x_host(x)
+    ref = O.quantize(xh, bits_np, 5150, 3, threads=CORES)
+    assert np.array_equal(host(p.packed[:int(ref[3][-1])]), ref[0])
+    exp = O.dequantize(*ref[:3], bits_np, N, D, out_dtype=O.F32, threads=CORES)
+    got = host(out).reshape(N, D).view(np.uint32)
+    if not np.array_equal(got, exp.view(np.uint32)):
+        bad = np.argwhere(got != exp.view(np.uint32))
+        raise AssertionError(f"{len(bad)} values differ, first {bad[:4].tolist()}")

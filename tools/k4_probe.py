@@ -54,5 +54,10 @@ pb, nb, sb = ps[big]
 algb = int(pb.off[-1].item()) + 8 * pb.zmin.numel() + 9 * pb.N + nb * sb
 res = {"config": cfg, "serial_ms": min(tot), "GBps_alg": alg / (min(tot) * 1e-3) / 1e9,
        "largest_us": per[big] * 1e3, "largest_GBps": algb / (per[big] * 1e-3) / 1e9,
-       "small_share": sum(t for t, (_, n, s) in zip(per, ps) if n * s < 120e6) / sum(per)}
+       "small_share": sum(t for t, (_, n, s) in zip(per, ps) if n * s < 120e6) / sum(per),
+       "small_ms": sum(t for t, (_, n, s) in zip(per, ps) if n * s < 120e6),
+       "large_ms": sum(t for t, (_, n, s) in zip(per, ps) if n * s >= 120e6)}
+if os.environ.get("PROBE_DUMP"):
+    res["layers"] = [[n * s, int(p.off[-1].item()) + 8 * p.zmin.numel() + 9 * p.N + n * s,
+                      round(t * 1e3, 2)] for (p, n, s), t in zip(ps, per)]
 print(json.dumps(res))

@@ -1,0 +1,6 @@
+for v in default storeonly nocompute nocomp_fake fake; do
+  L=paper_2104_14129_b200/libactnn.so; [ $v != default ] && L=paper_2104_14129_b200/csrc/build/var_$v/libactnn.so
+  for c in c3 c4; do
+    echo "$v $c $(PROBE_CONFIG=$c timeout 300 python tools/with_variant.py $L -- tools/k4_probe.py 2>&1 | tail -1)"
+  done
+done
