@@ -376,17 +376,16 @@ __device__ __forceinline__ uint32_t sr_code(float h, float Z, float inv14, uint3
 // on the ALU pipe -- no multiply, since the FMA-heavy pipe is the one the
 // Philox IMAD.WIDEs saturate.
 template <int b>
-__device__ __forceinline__ uint32_t codes_small(const float v[8], float Z, float inv14,
-                                                const Philox4& o) {
-    // scalar FADD/FFMA: measured ~6% faster per group than the f32x2 forms
+__device__ __forceinline__ uint32_t codes_small_d(const float d[8], float inv14, const Philox4& o) {
+    // scalar FFMA: measured ~6% faster per group than the f32x2 forms
     // (tools/cuda_checks/k3_compute.cu), which also compete with the Philox
     // IMAD.WIDEs for the FMA-heavy pipe
     const uint32_t w[4] = {o.x, o.y, o.z, o.w};
     uint32_t y = 0;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-        const float tx = __fmaf_rn(__fsub_rn(v[2 * p], Z), inv14, 12582912.0f);
-        const float ty = __fmaf_rn(__fsub_rn(v[2 * p + 1], Z), inv14, 12582912.0f);
+        const float tx = __fmaf_rn(d[2 * p], inv14, 12582912.0f);
+        const float ty = __fmaf_rn(d[2 * p + 1], inv14, 12582912.0f);
         uint32_t T = __byte_perm(__float_as_uint(tx), __float_as_uint(ty), 0x5410);
         T += w[p] & 0x3FFF3FFFu;
         if (b == 2)  // half 0 code -> bits 4p.., half 1 code -> bits 16 + 4p..
@@ -398,23 +397,69 @@ __device__ __forceinline__ uint32_t codes_small(const float v[8], float Z, float
     return (y | (y >> 15)) & 0xFFu;
 }
 
+// delta_j = RN(h_j - Z) (ACTNN-Q v1 O5) of a lane's 8 elements.
+// fp32: one FADD each.  bf16, from the raw bf16x2 words: the sm_100
+// mixed-precision subtract (sub.rn.f32.bf16 -> SASS FHADD.BF16, the bf16
+// operand taken from either register half) -- the bf16 value is exact in fp32
+// and the difference is rounded once, exactly as RN(float(h) - Z), with no
+// instruction spent on widening.
+__device__ __forceinline__ void deltas8(const float v[8], float Z, float d[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = __fsub_rn(v[j], Z);
+}
+__device__ __forceinline__ void sub_bf16x2(uint32_t w, float Z, float& d0, float& d1) {
+    asm("{\n.reg .b16 lo, hi;\nmov.b32 {lo, hi}, %2;\nsub.rn.f32.bf16 %0, lo, %3;\n"
+        "sub.rn.f32.bf16 %1, hi, %3;\n}\n"
+        : "=f"(d0), "=f"(d1)
+        : "r"(w), "f"(Z));
+}
+__device__ __forceinline__ void deltas8(const uint4& raw, float Z, float d[8]) {
+    sub_bf16x2(raw.x, Z, d[0], d[1]);
+    sub_bf16x2(raw.y, Z, d[2], d[3]);
+    sub_bf16x2(raw.z, Z, d[4], d[5]);
+    sub_bf16x2(raw.w, Z, d[6], d[7]);
+}
+
+// A lane's 8 elements as the consumer holds them: 8 widened fp32 values, or
+// (bf16 input) the 4 raw bf16x2 words of its 16-byte slice.
+struct F8 {
+    float v[8];
+};
+template <typename T>
+struct LaneIn;
+template <>
+struct LaneIn<float> {
+    using type = F8;
+};
+template <>
+struct LaneIn<uint16_t> {
+    using type = uint4;
+};
+__device__ __forceinline__ void deltas8(const F8& x, float Z, float d[8]) { deltas8(x.v, Z, d); }
+
+template <int b, typename In>
+__device__ __forceinline__ uint32_t codes_small(const In& x, float Z, float inv14,
+                                                const Philox4& o) {
+    float d[8];
+    deltas8(x, Z, d);
+    return codes_small_d<b>(d, inv14, o);
+}
+
 // Codes of one lane's 8 elements at b >= 3 (q up to 2^22, one code per
-// element; ACTNN-Q v1 O5-O7).  ACTNN_WIDE_F32X2=1 forms (h - Z) and the fma
-// against 1.5*2^23 two elements at a time with the sm_100 f32x2 instructions
-// (FADD2 / FFMA2: the same IEEE roundings per element as the scalar forms).
+// element; ACTNN-Q v1 O5-O7), from the deltas.  ACTNN_WIDE_F32X2=1 forms the
+// fma against 1.5*2^23 two elements at a time with the sm_100 f32x2 FFMA2
+// (the same IEEE rounding per element as the scalar form).
 #ifndef ACTNN_WIDE_F32X2
 #define ACTNN_WIDE_F32X2 0
 #endif
-__device__ __forceinline__ void codes_wide(const float v[8], float Z, float inv14,
-                                           const Philox4& o, uint32_t code[8]) {
+__device__ __forceinline__ void codes_wide_d(const float d[8], float inv14, const Philox4& o,
+                                             uint32_t code[8]) {
     const uint32_t w[4] = {o.x, o.y, o.z, o.w};
 #if ACTNN_WIDE_F32X2
-    const float2 nz = make_float2(-Z, -Z), iv = make_float2(inv14, inv14),
-                 mg = make_float2(12582912.0f, 12582912.0f);
+    const float2 iv = make_float2(inv14, inv14), mg = make_float2(12582912.0f, 12582912.0f);
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-        const float2 d = __fadd2_rn(make_float2(v[2 * p], v[2 * p + 1]), nz);
-        const float2 t = __ffma2_rn(d, iv, mg);
+        const float2 t = __ffma2_rn(make_float2(d[2 * p], d[2 * p + 1]), iv, mg);
         // the halves' bit patterns through an opaque move: with a plain
         // __float_as_uint, NVVM (CUDA 12.9) drops the shift that later places the
         // .x half's code into the packed word (tools/cuda_checks/f32x2_miscompile.cu)
@@ -428,9 +473,18 @@ __device__ __forceinline__ void codes_wide(const float v[8], float Z, float inv1
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const uint32_t r = ((j & 1) ? (w[j >> 1] >> 16) : w[j >> 1]) & 0x3FFFu;
-        code[j] = sr_code(v[j], Z, inv14, r);
+        const float t = __fmaf_rn(d[j], inv14, 12582912.0f);
+        code[j] = (__float_as_uint(t) - 0x4B400000u + r) >> 14;
     }
 #endif
+}
+
+template <typename In>
+__device__ __forceinline__ void codes_wide(const In& x, float Z, float inv14, const Philox4& o,
+                                           uint32_t code[8]) {
+    float d[8];
+    deltas8(x, Z, d);
+    codes_wide_d(d, inv14, o, code);
 }
 
 // ACTNN-Q v1 O10: h_hat = fmaf((float)code, scale, Z); (float)code is exact

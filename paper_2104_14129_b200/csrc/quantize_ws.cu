@@ -134,8 +134,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Codes of one group at width b from its Philox draw, packed and stored
 // (ACTNN-Q v1 O5-O8; the same arithmetic as quantize.cu).
-template <int b>
-__device__ __forceinline__ void ws_store(const float v[8], float Z, float inv14,
+template <int b, typename In>
+__device__ __forceinline__ void ws_store(const In& v, float Z, float inv14,
                                          const Philox4& o, uint8_t* seg, int lane) {
 #if ACTNN_WS_NARROW_ST
     // every lane stores its own b bytes: one warp store fills the group's
@@ -196,6 +196,11 @@ __device__ __forceinline__ void ws_store_any(int bw, const float v[8], float Z, 
     else if (bw == 7) ws_store<7>(v, Z, inv, o, sg, lane);
 }
 
+__device__ __forceinline__ void lane_load(const float* p, F8& x) { lds8(p, x.v); }
+__device__ __forceinline__ void lane_load(const uint16_t* p, uint4& x) {
+    x = *reinterpret_cast<const uint4*>(p);
+}
+
 // Lazy variant: each batch of PH groups is read from the stage just before it
 // is used, and the stage (data + descriptor) is released after the last
 // batch's reads -- only PH groups of data live in registers, which leaves room
@@ -215,11 +220,11 @@ __device__ __forceinline__ void ws_lazy_full(const T* st, const Desc& d, uint64_
     for (int q = 0; q < PH; ++q) o[q] = philox4x32_10_c32((uint32_t)(blk + (uint64_t)(q * 32)), rk);
 #pragma unroll
     for (int h = 0; h < U; h += PH) {
-        float v[PH][8];
+        typename LaneIn<T>::type v[PH];  // fp32: widened values; bf16: raw words
         float Z[PH], inv[PH];
 #pragma unroll
         for (int q = 0; q < PH; ++q) {
-            lds8(st + (h + q) * kG + lane * 8, v[q]);
+            lane_load(st + (h + q) * kG + lane * 8, v[q]);
             Z[q] = d.Z[h + q];
             inv[q] = d.inv[h + q];
         }
