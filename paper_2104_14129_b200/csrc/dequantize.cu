@@ -131,7 +131,19 @@ __device__ __forceinline__ uint32_t magic_code(uint64_t pay, int j) {
 // Shared-memory staging stores of a lane's 8 outputs.  fp32: two 16-byte
 // halves, the lanes of each quarter warp alternating which half goes first so
 // that every st.shared.v4 covers all 32 banks once; bf16: one 16-byte store.
+#ifndef ACTNN_DQ_STS_SWZ
+#define ACTNN_DQ_STS_SWZ 1
+#endif
 __device__ __forceinline__ void sts8(float* p, const float v[8]) {
+#if !ACTNN_DQ_STS_SWZ  // plain order: 2-way bank conflicts, no selects
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3])
+                 : "memory");
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p) + 16), "f"(v[4]),
+                 "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+    return;
+#endif
     const int lane = threadIdx.x & 31;
     const int h = (lane >> 2) & 1;
     const uint32_t a = smem_u32(p);

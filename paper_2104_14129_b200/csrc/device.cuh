@@ -437,6 +437,33 @@ struct LaneIn<uint16_t> {
 };
 __device__ __forceinline__ void deltas8(const F8& x, float Z, float d[8]) { deltas8(x.v, Z, d); }
 
+// A lane's 8 elements of a group from a shared-memory stage.
+__device__ __forceinline__ void lds8(const float* p, float v[8]);
+__device__ __forceinline__ void lane_load(const float* p, F8& x) { lds8(p, x.v); }
+__device__ __forceinline__ void lane_load(const uint16_t* p, uint4& x) {
+    x = *reinterpret_cast<const uint4*>(p);
+}
+
+// The lane's min / max of its 8 elements (exact selections; fp32 widened,
+// bf16 on packed bf16x2 halves, then widened exactly).
+__device__ __forceinline__ void lane_minmax(const F8& x, float& mn, float& mx) {
+    mn = x.v[0];
+    mx = x.v[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+        mn = fminf(mn, x.v[j]);
+        mx = fmaxf(mx, x.v[j]);
+    }
+}
+__device__ __forceinline__ uint32_t bmin2(uint32_t a, uint32_t b);
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b);
+__device__ __forceinline__ void lane_minmax(const uint4& w, float& mn, float& mx) {
+    const uint32_t mn2 = bmin2(bmin2(w.x, w.y), bmin2(w.z, w.w));
+    const uint32_t mx2 = bmax2(bmax2(w.x, w.y), bmax2(w.z, w.w));
+    mn = fminf(__uint_as_float(mn2 << 16), __uint_as_float(mn2 & 0xFFFF0000u));
+    mx = fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xFFFF0000u));
+}
+
 template <int b, typename In>
 __device__ __forceinline__ uint32_t codes_small(const In& x, float Z, float inv14,
                                                 const Philox4& o) {

@@ -11,18 +11,22 @@
 // of the group's 32 b-byte segment.
 //   - units are walked without division: (n, j) advances by the constant
 //     stride (nwarps / nb, nwarps % nb) with one carry;
-//   - group min/max (uniform single pass only): 8-element local min/max, then a
-//     5-step xor shuffle; in the mixed path (gmin, gmax) come from K1 and are
-//     prefetched one unit ahead;
+//   - group min/max (uniform single pass only): 8-element local min/max, then
+//     one redux.sync (CREDUX) each; in the mixed path (gmin, gmax) come from
+//     K1 and are prefetched one unit ahead (the mixed path normally runs the
+//     warp-specialised kernel of quantize_ws.cu instead);
 //   - per-group constants (two IEEE divisions) are computed lane-parallel, lane
 //     u for group u of the unit, and broadcast with one shuffle each;
-//   - arithmetic per element pair: one __fadd2_rn (h - Z) and one __ffma2_rn
-//     against 1.5*2^23 (f32x2, sm_100); for b <= 2 both codes are formed in the
-//     two 16-bit halves of one integer (q0 + r0 + ((q1 + r1) << 16), no carry as
-//     q + r < 2^16) and moved to their packed position with one IMAD.HI;
+//   - codes (device.cuh): delta = RN(h - Z) (FADD; bf16 via the mixed-precision
+//     FHADD.BF16), q from one scalar FFMA against 1.5*2^23; for b <= 2 two
+//     codes share one register (byte permute, one add of both 14-bit draws)
+//     and reach their packed bit positions by shifts and masks on the ALU pipe
+//     (no multiplies: the FMA-heavy pipe is the Philox one); b >= 3 one code per
+//     element;
 //   - Philox round keys live in the parameter constant bank (no key registers);
-//   - stores: b = 8 / 4 lanes write 8 / 4 bytes; b = 2 / 1 pair / quad lanes
-//     by shuffles so every store is a word and the warp fills whole sectors.
+//   - stores: every lane writes its own b code bytes (b <= 2: 1-2 bytes, b = 4
+//     / 8: one 4 / 8-byte word), so one warp store fills the group's 32 b-byte
+//     segment (whole sectors).
 // Ragged D, unaligned x or huge tensors take the generic kernel (scalar loads,
 // one group per warp iteration); it produces exactly the same bytes.
 #include <cstdlib>
@@ -138,8 +142,8 @@ __device__ __forceinline__ void group_const_store(float mn, float mx, int b, uin
 
 // One group: Philox draw for the lane's 8-element block, SR codes, pack, store
 // (ACTNN-Q v1 O6-O8).  seg = the group's 32 b-byte segment.
-template <int b>
-__device__ __forceinline__ void quant_group(const float v[8], float Z, float inv14, uint64_t blk,
+template <int b, typename In>
+__device__ __forceinline__ void quant_group(const In& v, float Z, float inv14, uint64_t blk,
                                             const RoundKeys& rk, uint8_t* seg, int lane) {
 #if ACTNN_Q_KEYS == 1
     const Philox4 o = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), rk.k[0], rk.k[1]);
@@ -176,8 +180,8 @@ __device__ __forceinline__ void quant_group(const float v[8], float Z, float inv
 
 // Width-dependent part of a unit: lane-parallel constants (lane u owns group
 // u of the unit), then codes + packing of each group.  kFullUnit: gcount == U.
-template <int b, bool kFullUnit>
-__device__ __forceinline__ void quant_unit(const float (&v)[kU][8], int gcount, float myMn,
+template <int b, bool kFullUnit, typename In>
+__device__ __forceinline__ void quant_unit(const In (&v)[kU], int gcount, float myMn,
                                            float myMx, float* zm, float* sc, uint32_t* mw,
                                            uint8_t* seg, uint64_t blk0, const RoundKeys& rk,
                                            int lane) {
@@ -195,8 +199,8 @@ __device__ __forceinline__ void quant_unit(const float (&v)[kU][8], int gcount, 
     }
 }
 
-template <int b>
-__device__ __forceinline__ void quant_unit_any(const float (&v)[kU][8], int gcount, float myMn,
+template <int b, typename In>
+__device__ __forceinline__ void quant_unit_any(const In (&v)[kU], int gcount, float myMn,
                                                float myMx, float* zm, float* sc, uint32_t* mw,
                                                uint8_t* seg, uint64_t blk0, const RoundKeys& rk,
                                                int lane) {
@@ -286,11 +290,12 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
         const int64_t sofs = kCached ? ((int64_t)s_off[n] << 5) : (p.off[n] - off0);
 
         mbar_wait(&bars[stage], phase);
-        float v[kU][8];
+        // a lane's 8 elements per group: widened fp32, or (bf16) the raw words
+        typename LaneIn<T>::type v[kU];
         const T* st = ring + stage * SE;
 #pragma unroll
         for (int k = 0; k < kU; ++k)
-            if (k < gcount) lds8(st + k * kG + lane * 8, v[k]);
+            if (k < gcount) lane_load(st + k * kG + lane * 8, v[k]);
         // Re-arm the stage with the unit S ahead as soon as it has been read, so
         // S units stay in flight while this one is computed.  Cross-proxy WAR
         // (generic-proxy shared loads, then an async-proxy bulk write to the same
@@ -312,12 +317,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
 #pragma unroll
             for (int k = 0; k < kU; ++k) {
                 if (k < gcount) {
-                    float mn = v[k][0], mx = v[k][0];
-#pragma unroll
-                    for (int jj = 1; jj < 8; ++jj) {
-                        mn = fminf(mn, v[k][jj]);
-                        mx = fmaxf(mx, v[k][jj]);
-                    }
+                    float mn, mx;
+                    lane_minmax(v[k], mn, mx);
                     mn = warp_min(mn);
                     mx = warp_max(mx);
                     if (lane == k) {

@@ -196,11 +196,6 @@ __device__ __forceinline__ void ws_store_any(int bw, const float v[8], float Z, 
     else if (bw == 7) ws_store<7>(v, Z, inv, o, sg, lane);
 }
 
-__device__ __forceinline__ void lane_load(const float* p, F8& x) { lds8(p, x.v); }
-__device__ __forceinline__ void lane_load(const uint16_t* p, uint4& x) {
-    x = *reinterpret_cast<const uint4*>(p);
-}
-
 // Lazy variant: each batch of PH groups is read from the stage just before it
 // is used, and the stage (data + descriptor) is released after the last
 // batch's reads -- only PH groups of data live in registers, which leaves room
