@@ -3,7 +3,10 @@
 //
 // A CTA = kCons consumer warps + kProd producer warps (each serving kCons/kProd
 // consumers; one producer warp per 8 consumers was latency-bound on its own
-// dependency chains at bf16, where a unit holds 8 groups).  Consumer warp w walks the
+// dependency chains at bf16, where a unit holds 8 groups).  Default: one CTA of
+// 16 consumers + 4 producers per SM, 2 stages per consumer (round 2: C3 step
+// 11.06 -> 10.49 ms and C4 step 53.5 -> 52.1 ms against two CTAs of 8 + 2 with 3
+// stages; the serial K3 time is 1-2% lower too).  Consumer warp w walks the
 // units u = (blockIdx * kCons + w) + r * nwarps (a unit = U consecutive groups
 // of one sample, 4 KB of input); it owns a ring of S shared-memory stages.
 // The producer warp, S rounds ahead of the consumers, for every consumer's
@@ -29,10 +32,10 @@ namespace actnn {
 namespace {
 
 #ifndef ACTNN_WS_CONS
-#define ACTNN_WS_CONS 8
+#define ACTNN_WS_CONS 16
 #endif
 #ifndef ACTNN_WS_S
-#define ACTNN_WS_S 3
+#define ACTNN_WS_S 2
 #endif
 #ifndef ACTNN_WS_PH
 #define ACTNN_WS_PH 2
@@ -44,7 +47,7 @@ namespace {
 #define ACTNN_WS_MD 1  // rounds of (gmin, gmax) prefetched by the producer (1-6 measured: 1 best)
 #endif
 #ifndef ACTNN_WS_MINB
-#define ACTNN_WS_MINB 2
+#define ACTNN_WS_MINB 1
 #endif
 #ifndef ACTNN_WS_PWAIT
 #define ACTNN_WS_PWAIT mbar_wait_sleep  // producer: sleep on the empty barrier
@@ -62,7 +65,7 @@ namespace {
 #define ACTNN_WS_CTAS_PER_SM 0  // 0: the occupancy limit
 #endif
 #ifndef ACTNN_WS_PROD
-#define ACTNN_WS_PROD 2
+#define ACTNN_WS_PROD 4
 #endif
 constexpr int kCons = ACTNN_WS_CONS;      // consumer warps per CTA
 constexpr int kProd = ACTNN_WS_PROD;      // producer warps per CTA (kCons / kProd consumers each)
