@@ -4,7 +4,7 @@
 # 2) --set full on the kernels of the largest C3 tensor (bn1 input, 822 MB fp32),
 # 3) --set full on the kernels of the largest C4 tensor (1.64 GB bf16),
 # 4) --set full on the NEXT-3 kernels (K6 grad_sqnorm, K5 stage-2 allocation).
-TAG=${1:-r01}
+TAG=${1:-r02}
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none -k regex:"group_stats|allocate|quantize|uniform|dequantize" -s 428 -c 428 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python tools/profile_step.py --steps 1 > gpurun_out/${TAG}_ncu_list.log 2>&1

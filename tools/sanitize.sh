@@ -5,6 +5,7 @@
 # mbarrier ordering).  Writes gpurun_out/sanitize_<tool>.log.
 CS=/usr/local/cuda/bin/compute-sanitizer
 SEL_Q='c1_golden or adversarial_all_widths or ragged or unaligned or empty or mixed_widths_multi_tile'
+SEL_F='tma_store_dequantize_large_fp32 and 2048'
 SEL_A='grad_sqnorm_edges or ema or stale or ties_and_edges or resnet50_parity'
 SEL_C='relu_pack_and_backward and 1023 or maxpool_forward_backward'
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
@@ -16,6 +17,8 @@ for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
     tail -6 gpurun_out/sanitize_${tool}_q_full.log
     echo "hazard sites (kernel, source line):"
     grep -o "Race reported between.*" gpurun_out/sanitize_${tool}_q_full.log | sed 's/+0x[0-9a-f]*//g' | sort | uniq -c | sort -rn | head -20
+    echo "### TMA-store K4 (205 MB fp32 output) and uncached kernels"
+    timeout 1500 $CS --tool $tool $extra --print-limit 20 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_full_parity.py -k "$SEL_F or (uncached_variants and 1280)" 2>&1 | tail -4
     timeout 1500 $CS --tool $tool $extra --print-limit 20 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_adapt.py -k "$SEL_A" 2>&1 | tail -4
     timeout 1500 $CS --tool $tool $extra --print-limit 20 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_contexts.py -k "$SEL_C" 2>&1 | tail -4
     if [ "$tool" = "racecheck" ]; then
