@@ -375,12 +375,60 @@ __device__ __forceinline__ uint32_t sr_code(float h, float Z, float inv14, uint3
 // packed positions (element j at bits [j b, (j + 1) b)) with shifts and masks
 // on the ALU pipe -- no multiply, since the FMA-heavy pipe is the one the
 // Philox IMAD.WIDEs saturate.
+//
+// ACTNN_PACK_MUL=1 (default) gathers the codes with byte permutes and one
+// multiply instead of a shift + mask per register pair (4-6 fewer ALU
+// instructions per group; on sm_100 the ALU instructions and the Philox
+// IMAD.WIDEs add up rather than overlap, tools/cuda_checks/k3_mix.cu):
+//   b = 1: the fma uses the magic 1.5 2^23 + 2^14 (still even, so ties are
+//   unchanged), so each half holds q + r + 2^14 < 2^16 and its bit 15 (the
+//   byte's sign bit) is the code [q + r >= 2^14].  A sign-replicating byte
+//   permute turns the four codes of two registers into 0x00 / 0xFF bytes;
+//   element j keeps bit j (j < 4 from the first permute, j >= 4 from the
+//   second), and one multiply by 0x01010101 ORs the four disjoint bytes into
+//   the top byte.
+//   b = 2: a byte permute collects bits 14-15 / 30-31 of two registers as
+//   bits 6-7 of four bytes (element k at 6 + 8k); times 1 + 2^6 + 2^12 + 2^18
+//   moves element k to bits 24 + 2k (every other partial product lands in a
+//   disjoint 2-bit field below bit 24 or above bit 31, so nothing carries);
+//   a final permute joins the two top bytes.
+#ifndef ACTNN_PACK_MUL
+#define ACTNN_PACK_MUL 1
+#endif
+// prmt with sign-replicating selector nibbles (bit 3 of a nibble set: the
+// selected byte's sign bit fills the output byte).  __byte_perm ignores that
+// bit (CUDA masks each selector nibble to 3 bits), hence the inline PTX.
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
 template <int b>
 __device__ __forceinline__ uint32_t codes_small_d(const float d[8], float inv14, const Philox4& o) {
     // scalar FFMA: measured ~6% faster per group than the f32x2 forms
     // (tools/cuda_checks/k3_compute.cu), which also compete with the Philox
     // IMAD.WIDEs for the FMA-heavy pipe
     const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#if ACTNN_PACK_MUL
+    uint32_t T[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const float magic = b == 1 ? 12599296.0f : 12582912.0f;  // 1.5 2^23 (+ 2^14)
+        const float tx = __fmaf_rn(d[2 * p], inv14, magic);
+        const float ty = __fmaf_rn(d[2 * p + 1], inv14, magic);
+        T[p] = __byte_perm(__float_as_uint(tx), __float_as_uint(ty), 0x5410) +
+               (w[p] & 0x3FFF3FFFu);
+    }
+    if (b == 1) {
+        const uint32_t A = prmt_sign(T[0], T[1], 0xFDB9);  // elements 0-3: 0x00 / 0xFF
+        const uint32_t B = prmt_sign(T[2], T[3], 0xFDB9);  // elements 4-7
+        const uint32_t X = ((A & 0x0F0F0F0Fu) | (B & 0xF0F0F0F0u)) & 0x88442211u;
+        return (X * 0x01010101u) >> 24;
+    }
+    const uint32_t A = __byte_perm(T[0], T[1], 0x7531) & 0xC0C0C0C0u;
+    const uint32_t B = __byte_perm(T[2], T[3], 0x7531) & 0xC0C0C0C0u;
+    return __byte_perm(A * 0x00041041u, B * 0x00041041u, 0x0073) & 0xFFFFu;
+#else
     uint32_t y = 0;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -395,6 +443,7 @@ __device__ __forceinline__ uint32_t codes_small_d(const float d[8], float inv14,
     }
     if (b == 2) return (y | (y >> 14)) & 0xFFFFu;
     return (y | (y >> 15)) & 0xFFu;
+#endif
 }
 
 // delta_j = RN(h_j - Z) (ACTNN-Q v1 O5) of a lane's 8 elements.

@@ -12,7 +12,9 @@
 //   - units are walked without division: (n, j) advances by the constant
 //     stride (nwarps / nb, nwarps % nb) with one carry;
 //   - group min/max (uniform single pass only): 8-element local min/max, then
-//     one redux.sync (CREDUX) each; in the mixed path (gmin, gmax) come from
+//     one redux.sync (CREDUX) each; a full unit at width 1/2/4/8 runs straight
+//     line (sp_full_unit: its Philox draws issued first, no per-group
+//     branches); in the mixed path (gmin, gmax) come from
 //     K1 and are prefetched one unit ahead (the mixed path normally runs the
 //     warp-specialised kernel of quantize_ws.cu instead);
 //   - per-group constants (two IEEE divisions) are computed lane-parallel, lane
@@ -20,9 +22,8 @@
 //   - codes (device.cuh): delta = RN(h - Z) (FADD; bf16 via the mixed-precision
 //     FHADD.BF16), q from one scalar FFMA against 1.5*2^23; for b <= 2 two
 //     codes share one register (byte permute, one add of both 14-bit draws)
-//     and reach their packed bit positions by shifts and masks on the ALU pipe
-//     (no multiplies: the FMA-heavy pipe is the Philox one); b >= 3 one code per
-//     element;
+//     and are gathered into the packed byte / half-word by byte permutes and one
+//     multiply (device.cuh codes_small_d); b >= 3 one code per element;
 //   - Philox round keys live in the parameter constant bank (no key registers);
 //   - stores: every lane writes its own b code bytes (b <= 2: 1-2 bytes, b = 4
 //     / 8: one 4 / 8-byte word), so one warp store fills the group's 32 b-byte
@@ -52,11 +53,14 @@ constexpr unsigned kFull = 0xffffffffu;
 
 template <typename T>
 struct Cfg;
+// fp32: 2 CTAs of 8 warps per SM with 3 stages each (round 2, with the
+// straight-line full-unit single pass: C2 K3 178 -> 168 us; 3 CTAs x 2 stages
+// leaves that path 80 registers and spills)
 #ifndef ACTNN_Q_S32
-#define ACTNN_Q_S32 2
+#define ACTNN_Q_S32 3
 #endif
 #ifndef ACTNN_Q_MINB32
-#define ACTNN_Q_MINB32 3
+#define ACTNN_Q_MINB32 2
 #endif
 #ifndef ACTNN_Q_S16
 #define ACTNN_Q_S16 4
@@ -210,6 +214,75 @@ __device__ __forceinline__ void quant_unit_any(const In (&v)[kU], int gcount, fl
         quant_unit<b, false>(v, gcount, myMn, myMx, zm, sc, mw, seg, blk0, rk, lane);
 }
 
+// Full unit (gcount == U) of the single pass (statistics in-kernel), straight
+// line with no per-group branches.  The Philox draws depend only on the unit
+// index, so they are issued first: their ten-round IMAD.WIDE chains overlap
+// the statistics' dependency chain (lane min/max -> CREDUX -> lane-parallel
+// divisions -> shuffles) instead of waiting behind it.
+#ifndef ACTNN_SP_FULL
+#define ACTNN_SP_FULL 1
+#endif
+#ifndef ACTNN_SP_HOIST
+#define ACTNN_SP_HOIST 1  // 0: each group's Philox draw just before its codes
+#endif
+template <int b, typename In>
+__device__ __forceinline__ void sp_full_unit(const In (&v)[kU], float* zm, float* sc,
+                                             uint32_t* mw, uint8_t* seg, uint64_t blk0,
+                                             const RoundKeys& rk, int lane) {
+    Philox4 o[kU];
+#if ACTNN_SP_HOIST
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+        o[u] = philox4x32_10_c32((uint32_t)(blk0 + (uint64_t)(u * 32 + lane)), rk);
+#endif
+    float gmn[kU], gmx[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        float mn, mx;
+        lane_minmax(v[u], mn, mx);
+        gmn[u] = warp_min(mn);
+        gmx[u] = warp_max(mx);
+    }
+    // lane u (< U) computes group u's constants
+    float myMn = gmn[0], myMx = gmx[0];
+#pragma unroll
+    for (int u = 1; u < kU; ++u) {
+        myMn = lane == u ? gmn[u] : myMn;
+        myMx = lane == u ? gmx[u] : myMx;
+    }
+    float cZ, cInv;
+    group_const_store(myMn, myMx, b, mw ? mw + lane : nullptr, zm + lane, sc + lane, lane < kU,
+                      cZ, cInv);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const float Z = __shfl_sync(kFull, cZ, u);
+        const float inv = __shfl_sync(kFull, cInv, u);
+#if !ACTNN_SP_HOIST
+        o[u] = philox4x32_10_c32((uint32_t)(blk0 + (uint64_t)(u * 32 + lane)), rk);
+#endif
+        uint8_t* sg = seg + u * 32 * b;
+        if constexpr (b == 2) {
+            reinterpret_cast<uint16_t*>(sg)[lane] = (uint16_t)codes_small<2>(v[u], Z, inv, o[u]);
+        } else if constexpr (b == 1) {
+            sg[lane] = (uint8_t)codes_small<1>(v[u], Z, inv, o[u]);
+        } else {
+            uint32_t code[8];
+            codes_wide(v[u], Z, inv, o[u], code);
+            if constexpr (b == 8) {
+                const uint32_t lo = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
+                const uint32_t hi = code[4] | (code[5] << 8) | (code[6] << 16) | (code[7] << 24);
+                *reinterpret_cast<uint2*>(sg + lane * 8) = make_uint2(lo, hi);
+            } else {
+                static_assert(b == 4, "full-unit widths: 1, 2, 4, 8");
+                uint32_t pl = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) pl |= code[j] << (4 * j);
+                *reinterpret_cast<uint32_t*>(sg + lane * 4) = pl;
+            }
+        }
+    }
+}
+
 template <typename T, bool kStats, bool kCached>
 __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
     quantize_fast_kernel(const __grid_constant__ QParams p) {
@@ -312,6 +385,26 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
                          bytes, &bars[stage]);
             }
             advance(pn, pj);
+        }
+        if constexpr (kStats && ACTNN_SP_FULL) {
+            if (gcount == kU && (b == 1 || b == 2 || b == 4 || b == 8)) {
+                uint8_t* seg = p.packed + sofs + (uint64_t)gi * 32 * b;
+                const uint64_t blk0 = (uint64_t)(p.sample_base + n) * (p.D >> 3) + (uint64_t)gi * 32;
+                float* zm = p.zmin + g;
+                float* sc = p.scale + g;
+                uint32_t* mw = p.meta ? p.meta + g : nullptr;
+                if (b == 2) sp_full_unit<2>(v, zm, sc, mw, seg, blk0, p.rk, lane);
+                else if (b == 1) sp_full_unit<1>(v, zm, sc, mw, seg, blk0, p.rk, lane);
+                else if (b == 4) sp_full_unit<4>(v, zm, sc, mw, seg, blk0, p.rk, lane);
+                else sp_full_unit<8>(v, zm, sc, mw, seg, blk0, p.rk, lane);
+                if (++stage == S) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+                n = nn;
+                j = nj;
+                continue;
+            }
         }
         if constexpr (kStats) {
 #pragma unroll

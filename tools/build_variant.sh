@@ -14,5 +14,5 @@ for f in abi quantize quantize_ws dequantize stats allocate contexts adapt; do
   $NV -O3 -std=c++17 $A -lineinfo -fmad=false -Xcompiler -fPIC,-O2 -Xptxas -v $FLAGS -c $f.cu -o $D/$f.o 2> $D/$f.ptxas.txt &
 done
 wait
-$NV $A -shared -o $D/libactnn.so $D/*.o && find $D -name "*.o" ! -name "quantize_ws.o" ! -name "dequantize.o" -delete
+$NV $A -shared -o $D/libactnn.so $D/*.o && find $D -name "*.o" -delete
 echo "$D/libactnn.so ($FLAGS)"
