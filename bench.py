@@ -387,9 +387,18 @@ class Run:
         return t_comp, t_decomp
 
     def breakdown(self, torch, barrier, kb):
-        """Serial per-kernel breakdown: every tensor's launches back to back on
-        the main stream, an event pair around each kernel.  A spin kernel ahead
-        of each pass keeps host enqueue gaps out of the events."""
+        """Serial per-kernel breakdown, two ways, both on the main stream with a
+        spin kernel ahead of each pass (host enqueue gaps stay out of the events):
+          - kernel-major sequence (the roofline's launch durations): K1 of every
+            tensor back to back, then every [all-gather +] K2, every K3, every K4,
+            one event pair around each kernel type's run of launches; a kernel's
+            average launch duration = its run / the number of launches.  Each
+            launch still runs alone (same stream, no overlap), ramp and tail
+            included;
+          - an event pair around every single launch (tensor-major order), which
+            adds the per-event-pair overhead (~4-6 us measured on this part:
+            tools/cuda_checks/small_write.cu times an empty kernel at 6 us) to
+            every launch; kept as `per_launch_event_pairs` for comparison."""
         import ctypes
         plan, outs, out_dt = self.plan, self.outs, self.out_dt
         sp = ctypes.c_void_p(self.ps.stream.cuda_stream)
@@ -406,6 +415,29 @@ class Run:
             for i in range(nl):
                 plan.decompress_layer(i, outs[i & 1], out_dt, sp, ev[nl + i])
 
+        lib = plan.lib
+        from paper_2104_14129_b200 import plan as plan_mod
+        _lib_check, _ptr = plan_mod._lib.check, plan_mod._p
+
+        def sequence(ev):
+            ev[0].record()
+            if plan.mixed:
+                for L in plan.layers:
+                    _lib_check(lib.actnn_group_stats(*L.args["stats"], sp))
+            ev[1].record()
+            if plan.mixed:
+                for L in plan.layers:
+                    if plan.gather is not None:
+                        plan.gather(L.S, L.S_loc)
+                    _lib_check(lib.actnn_allocate_bits(*L.args["alloc"], sp))
+            ev[2].record()
+            for L in plan.layers:
+                _lib_check(plan.qfn(*L.args["quant"], sp))
+            ev[3].record()
+            for i, L in enumerate(plan.layers):
+                _lib_check(plan.dfn(*L.args["dequant"], _ptr(outs[i & 1]), out_dt, sp))
+            ev[4].record()
+
         with torch.cuda.stream(self.ps.stream):
             barrier()
             t_host = time.perf_counter()
@@ -419,6 +451,20 @@ class Run:
                 serial(ev)
                 evs.append(ev)
             barrier()
+            seqs = []
+            for _ in range(kb):
+                torch.cuda._sleep(int(1.5 * t_host * 2.0e9))
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                sequence(ev)
+                seqs.append(ev)
+            barrier()
+        kseq = {"stats": 0.0, "quantize": 0.0, "dequantize": 0.0}
+        for ev in seqs:
+            if plan.mixed:
+                kseq["stats"] += ev[0].elapsed_time(ev[1])
+            kseq["quantize"] += ev[2].elapsed_time(ev[3])
+            kseq["dequantize"] += ev[3].elapsed_time(ev[4])
+        self.kt_seq = {k: v / kb for k, v in kseq.items()}
         kt = {"stats": 0.0, "quantize": 0.0, "dequantize": 0.0}
         tq = {"compress": 0.0, "decompress": 0.0}
         for per in evs:
@@ -448,6 +494,10 @@ class Run:
         alg = algorithmic_bytes(plan.layers, bits_host, self.s_in, self.s_in, plan.mixed,
                                 4 if args.meta == "bf16" else 8)
         nl = len(plan.layers)
+        # launch durations from the kernel-major sequence (breakdown docstring);
+        # the per-launch event-pair numbers ride along for comparison
+        kev = kt
+        kt = getattr(self, "kt_seq", None) or kev
         dom = max(kt, key=lambda k: kt[k])
         ach = alg[dom] / (kt[dom] * 1e-3) / 1e9
         names = {"stats": "group_stats_kernel (K1)",
@@ -463,6 +513,9 @@ class Run:
                         and self.pool == 0 else None),
             "algorithmic_bytes_per_launch": alg[dom] / nl,
             "avg_launch_us": kt[dom] * 1e3 / nl,
+            "launch_timing": "kernel-major sequence: one event pair around the run of all "
+                             f"{nl} launches of the kernel on its stream, each launch alone",
+            "avg_launch_us_event_pairs": kev[dom] * 1e3 / nl,
             "launches_per_step": nl,
             # the same kernel inside the timed schedule: K4 is the only kernel of
             # the decompress phase (its launches overlap on several streams)
@@ -477,7 +530,10 @@ class Run:
                                "frac": (alg[k] / (kt[k] * 1e-3) / 1e9 / peak) if kt[k] else None,
                                "frac_nominal": (alg[k] / (kt[k] * 1e-3) / 1e9 / NOMINAL_HBM_GBS)
                                if kt[k] else None,
-                               "algorithmic_bytes_per_step": alg[k]}
+                               "algorithmic_bytes_per_step": alg[k],
+                               "ms_per_step_event_pairs": kev[k],
+                               "frac_event_pairs": (alg[k] / (kev[k] * 1e-3) / 1e9 / peak)
+                               if kev[k] else None}
                            for k in kt}}
         total_alg = sum(alg.values())
         avg_bits = [float(b.double().mean()) for b in bits_host]
