@@ -67,6 +67,22 @@ MIX(m_wide_ffma2, wide(a[i], b[i]); ffma2(f[i], g[i], 1.0001f);)
 MIX(m_imadlo, imadlo(a[i], b[i]);)
 MIX(m_imadhi, imadhi(a[i], b[i]);)
 MIX(m_wide_lop1, wide(a[i], b[i]); lop(b[i], a[i]);)
+__device__ __forceinline__ void hilo(uint32_t& a, uint32_t& b) {  // IMAD.HI + IMAD instead of IMAD.WIDE
+    uint32_t h, l;
+    asm volatile("mul.hi.u32 %0, %1, 0xD2511F53;" : "=r"(h) : "r"(a));
+    asm volatile("mul.lo.u32 %0, %1, 0xD2511F53;" : "=r"(l) : "r"(a));
+    a = l;
+    b ^= h;
+}
+__device__ __forceinline__ void hionly(uint32_t& a) {
+    asm volatile("mul.hi.u32 %0, %0, 0xD2511F53;" : "+r"(a));
+}
+MIX(m_hilo, hilo(a[i], b[i]);)
+MIX(m_hilo_lop, hilo(a[i], b[i]); lop(b[i], a[i]);)
+MIX(m_hionly, hionly(a[i]);)
+MIX(m_hionly_lop, hionly(a[i]); lop(b[i], a[i]);)
+MIX(m_imadlo_lop, imadlo(a[i], b[i]); lop(b[i], a[i]);)
+MIX(m_wide_2ffma_lop, wide(a[i], b[i]); ffma_imm(f[i], g[i]); ffma_imm(g[i], f[i]); lop(b[i], a[i]);)
 MIX(m_lop, lop(a[i], b[i]);)
 MIX(m_ffma, ffma_imm(f[i], g[i]);)
 MIX(m_fhadd, fhadd(f[i], a[i]);)
@@ -194,6 +210,7 @@ int main() {
         T(m_wide) T(m_lop) T(m_ffma) T(m_fhadd) T(m_iadd) T(m_wide_lop2) T(m_wide_ffma)
         T(m_wide_ffma2x) T(m_wide_fhadd) T(m_wide_iadd) T(m_lop_ffma) T(m_lop_fhadd)
         T(m_ffma2) T(m_wide_ffma2) T(m_imadlo) T(m_imadhi) T(m_wide_lop1)
+        T(m_hilo) T(m_hilo_lop) T(m_hionly) T(m_hionly_lop) T(m_imadlo_lop) T(m_wide_2ffma_lop)
         P pp;
         pp.rk = make_round_keys(42);
         const uint32_t groups = 512;

@@ -61,3 +61,27 @@ if os.environ.get("PROBE_DUMP"):
     res["layers"] = [[n * s, int(p.off[-1].item()) + 8 * p.zmin.numel() + 9 * p.N + n * s,
                       round(t * 1e3, 2)] for (p, n, s), t in zip(ps, per)]
 print(json.dumps(res))
+
+# per size class: 8 back-to-back launches of one tensor of the class between one
+# event pair (no per-launch event overhead), best of 3
+if os.environ.get("PROBE_SIZES"):
+    seen = {}
+    for i, (p, n, s) in enumerate(ps):
+        seen.setdefault(n * s, i)
+    rows = []
+    for nbytes, i in sorted(seen.items()):
+        p, n, s = ps[i]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e9
+        for _ in range(3):
+            torch.cuda._sleep(20_000_000)
+            a.record()
+            for _ in range(8):
+                A.dequantize(p, out=out[:n].view(p.shape))
+            b.record()
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b) / 8)
+        algi = int(p.off[-1].item()) + 8 * p.zmin.numel() + 9 * p.N + n * s
+        rows.append([round(nbytes / 1e6, 1), sum(1 for _, m, t in ps if m * t == nbytes),
+                     round(best * 1e3, 1), round(algi / (best * 1e-3) / 1e9)])
+    print(json.dumps({"config": cfg, "sizes_MB_count_us_GBps": rows}))
