@@ -97,6 +97,8 @@ __device__ __forceinline__ long long block_excl_scan(long long v, Shared& sh, lo
 }
 
 __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
+    pdl_trigger();  // the next kernel of the stream may start launching
+    pdl_wait();     // the previous grid is complete and visible
     __shared__ Shared sh;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int M = p.M;
@@ -333,7 +335,7 @@ cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s) {
     p.unit = a.unit;
     p.bits = a.bits;
     p.off = a.off;
-    allocate_kernel<<<1, kThreads, 0, s>>>(p);
+    launch_pdl(allocate_kernel, 1, kThreads, 0, s, p);
     return cudaGetLastError();
 }
 

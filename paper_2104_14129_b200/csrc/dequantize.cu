@@ -237,6 +237,8 @@ __device__ __forceinline__ void dequant_unit_any(const uint8_t* st, int gcount,
 template <typename TO, bool kCached, bool kMeta, bool kB16, bool kTS>
 __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACTNN_DQ_MINB)
     dequantize_fast_kernel(const __grid_constant__ DParams p) {
+    pdl_trigger();  // the next kernel of the stream may start launching
+    pdl_wait();     // the previous grid is complete and visible
     constexpr int kW = warps<kTS>();
     extern __shared__ __align__(128) uint8_t smem[];
     TO* stg = reinterpret_cast<TO*>(smem + stg_off<kTS>()) + (size_t)(threadIdx.x >> 5) * kO * kU * kG;
@@ -414,6 +416,8 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
 // Generic path: ragged last group / unaligned output; one group per warp.
 template <typename TO>
 __global__ void __launch_bounds__(kBlock) dequantize_generic_kernel(const __grid_constant__ GDParams p) {
+    pdl_trigger();  // the next kernel of the stream may start launching
+    pdl_wait();     // the previous grid is complete and visible
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -459,7 +463,7 @@ void launch_fast_t(const DParams& p0, int64_t units, cudaStream_t s) {
     const uint32_t nwarps = (uint32_t)grid * kW;
     p.step_n = nwarps / p.nb;
     p.step_j = nwarps % p.nb;
-    dequantize_fast_kernel<TO, kCached, kMeta, kB16, kTS><<<grid, kW * 32, kSmem, s>>>(p);
+    launch_pdl(dequantize_fast_kernel<TO, kCached, kMeta, kB16, kTS>, grid, kW * 32, kSmem, s, p);
 }
 
 template <typename TO, bool kCached, bool kMeta, bool kB16>
@@ -513,7 +517,7 @@ cudaError_t run(const DequantArgs& a, cudaStream_t s) {
         GDParams p{a.packed, a.zmin, a.scale, a.meta, a.bits, a.off, a.N, a.D, a.ng, a.out};
         const int grid = grid_for((const void*)dequantize_generic_kernel<TO>, kBlock, 0,
                                   (a.N * a.ng + kWarps - 1) / kWarps);
-        dequantize_generic_kernel<TO><<<grid, kBlock, 0, s>>>(p);
+        launch_pdl(dequantize_generic_kernel<TO>, grid, kBlock, 0, s, p);
     }
     return cudaGetLastError();
 }

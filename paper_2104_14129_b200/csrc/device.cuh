@@ -15,6 +15,28 @@ namespace actnn {
 #endif
 
 constexpr int kG = 256;            // group size ("we set G = 256")
+
+// ------------------------------------------- programmatic dependent launch
+// The hot-path kernels are launched with programmatic stream serialization
+// (launch.h launch_pdl): each CTA first lets the next kernel of its stream
+// start launching (its CTAs take SM slots as this grid's CTAs retire, so the
+// launch latency and its prologue overlap this grid's tail), and waits for the
+// previous grid to complete -- with all its memory operations visible -- before
+// its own first global memory access.  Without the launch attribute both are
+// no-ops.
+#ifndef ACTNN_PDL
+#define ACTNN_PDL 1
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if ACTNN_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if ACTNN_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 constexpr int kWarp = 32;
 constexpr int kElemsPerLane = 8;   // kG / kWarp: one Philox call per lane per group
 constexpr int kChunk = 32;         // groups per tile = one group per lane for metadata

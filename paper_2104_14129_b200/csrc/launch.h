@@ -142,4 +142,29 @@ int grid_for(const void* kernel, int block, size_t smem, int64_t work_blocks);
 // per (kernel, device) (thread-safe; several GPUs in one process are fine).
 void ensure_smem_attr(const void* kernel, size_t bytes);
 
+// Launch with programmatic stream serialization (device.cuh pdl_trigger /
+// pdl_wait: only for kernels that wait before touching global memory).
+#ifndef ACTNN_PDL
+#define ACTNN_PDL 1
+#endif
+template <typename... P, typename... A>
+inline void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       A... args) {
+#if ACTNN_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+#else
+    kernel<<<grid, block, smem, s>>>(args...);
+#endif
+}
+
 }  // namespace actnn

@@ -286,6 +286,8 @@ __device__ __forceinline__ void sp_full_unit(const In (&v)[kU], float* zm, float
 template <typename T, bool kStats, bool kCached>
 __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
     quantize_fast_kernel(const __grid_constant__ QParams p) {
+    pdl_trigger();  // the next kernel of the stream may start launching
+    pdl_wait();     // the previous grid is complete and visible
     constexpr int S = Cfg<T>::S;
     constexpr int SE = stage_bytes<T>() / (int)sizeof(T);  // elements per stage
     extern __shared__ __align__(128) uint8_t smem[];
@@ -456,6 +458,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<T>::MinBlocks)
 // lane needs at most two blocks when D % 8 != 0.
 template <typename T, bool kStats>
 __global__ void __launch_bounds__(kBlock) quantize_generic_kernel(const __grid_constant__ GParams p) {
+    pdl_trigger();  // the next kernel of the stream may start launching
+    pdl_wait();     // the previous grid is complete and visible
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * kBlock) >> 5;
@@ -548,9 +552,9 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
         p.step_n = nwarps / p.nb;
         p.step_j = nwarps % p.nb;
         if (cached)
-            quantize_fast_kernel<T, kStats, true><<<grid, kBlock, smem_bytes<T>(), s>>>(p);
+            launch_pdl(quantize_fast_kernel<T, kStats, true>, grid, kBlock, smem_bytes<T>(), s, p);
         else
-            quantize_fast_kernel<T, kStats, false><<<grid, kBlock, smem_bytes<T>(), s>>>(p);
+            launch_pdl(quantize_fast_kernel<T, kStats, false>, grid, kBlock, smem_bytes<T>(), s, p);
     } else {
         GParams p;
         p.x = a.x;
@@ -569,7 +573,7 @@ cudaError_t run(const QuantArgs& a, cudaStream_t s) {
         p.rk = make_round_keys(a.seed);
         const void* k = (const void*)quantize_generic_kernel<T, kStats>;
         const int grid = grid_for(k, kBlock, 0, (a.N * a.ng + kWarps - 1) / kWarps);
-        quantize_generic_kernel<T, kStats><<<grid, kBlock, 0, s>>>(p);
+        launch_pdl(quantize_generic_kernel<T, kStats>, grid, kBlock, 0, s, p);
     }
     return cudaGetLastError();
 }

@@ -483,6 +483,8 @@ __device__ __forceinline__ void ws_unit_packed(const uint16_t* st, const Desc& d
 
 template <typename T, bool kCached>
 __global__ void __launch_bounds__(kThreads, ACTNN_WS_MINB) quantize_ws_kernel(const __grid_constant__ WSParams p) {
+    pdl_trigger();  // the next kernel of the stream may start launching
+    pdl_wait();     // the previous grid is complete and visible
     constexpr int U = WS<T>::U;
     constexpr int SE = WS<T>::SE;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -670,7 +672,7 @@ void launch_ws(WSParams p, int64_t units, cudaStream_t s) {
     const uint32_t nwarps = (uint32_t)grid * kCons;
     p.step_n = nwarps / p.nb;
     p.step_j = nwarps % p.nb;
-    quantize_ws_kernel<T, kCached><<<grid, kThreads, ws_smem_bytes<T>(), s>>>(p);
+    launch_pdl(quantize_ws_kernel<T, kCached>, grid, kThreads, ws_smem_bytes<T>(), s, p);
 }
 
 template <typename T>

@@ -64,6 +64,8 @@ __device__ __forceinline__ uint4 ldg_nc_u4(const uint16_t* p) {
 
 template <typename T, bool kFast>
 __global__ void __launch_bounds__(SCfg<T>::Block) group_stats_kernel(SParams p) {
+    pdl_trigger();  // the next kernel of the stream may start launching
+    pdl_wait();     // the previous grid is complete and visible
     constexpr int kU = SCfg<T>::U;
     constexpr int kBlock = SCfg<T>::Block;
     __shared__ float sZ[kChunk], sM[kChunk];
@@ -211,10 +213,10 @@ cudaError_t run(const StatsArgs& a, cudaStream_t s) {
         const int cap_per_sm = ACTNN_K1_CTAS_PER_SM >= 0 ? ACTNN_K1_CTAS_PER_SM
                                                          : (sizeof(T) == 4 ? 4 : 0);
         if (cap_per_sm > 0 && grid > sm_count() * cap_per_sm) grid = sm_count() * cap_per_sm;
-        group_stats_kernel<T, true><<<grid, SCfg<T>::Block, 0, s>>>(p);
+        launch_pdl(group_stats_kernel<T, true>, grid, SCfg<T>::Block, 0, s, p);
     } else {
         const int grid = grid_for((const void*)group_stats_kernel<T, false>, SCfg<T>::Block, 0, tiles);
-        group_stats_kernel<T, false><<<grid, SCfg<T>::Block, 0, s>>>(p);
+        launch_pdl(group_stats_kernel<T, false>, grid, SCfg<T>::Block, 0, s, p);
     }
     return cudaGetLastError();
 }

@@ -9,6 +9,16 @@
 
 __global__ void empty_k() {}
 
+// PDL: let the next launch in the stream start (griddepcontrol.launch_dependents),
+// then wait for the previous grid's completion before touching memory
+__global__ void write_pdl_k(float4* out, size_t n4) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
+        out[i] = make_float4(1.f, 2.f, 3.f, (float)i);
+}
+
 __global__ void write_k(float4* out, size_t n4) {
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
@@ -47,6 +57,33 @@ int main() {
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
         printf("empty kernel: %.2f us\n", ms * 1e3);
+    }
+    // back-to-back launches in one stream, one event pair around 8 of them
+    for (double mb : {0.0, 2.1, 25.7, 102.8}) {
+        const size_t n4 = (size_t)(mb * 1e6) / 16;
+        for (int pdl = 0; pdl < 2; ++pdl) {
+            float best = 1e9;
+            for (int r = 0; r < 5; ++r) {
+                cudaEventRecord(e0);
+                for (int k = 0; k < 8; ++k) {
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3(sms * 8);
+                    cfg.blockDim = dim3(256);
+                    cfg.stream = 0;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    at[0].val.programmaticStreamSerializationAllowed = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = pdl;
+                    cudaLaunchKernelEx(&cfg, write_pdl_k, out, n4);
+                }
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            printf("sequence of 8: %6.1f MB writes, PDL %d: %.2f us per launch\n", mb, pdl, best * 1e3 / 8);
+        }
     }
     for (double mb : {25.7, 51.4, 102.8, 205.5, 822.1}) {
         const size_t n4 = (size_t)(mb * 1e6) / 16;
