@@ -126,6 +126,7 @@ cudaError_t launch_maxpool2d(const PoolArgs& a, bool backward, cudaStream_t s);
 
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s);
 cudaError_t launch_quantize_ws(const QuantArgs& a, cudaStream_t s);  // mixed-mode fast path
+cudaError_t launch_quantize_sp8(const QuantArgs& a, cudaStream_t s);  // fp32 single pass, 8-group units
 cudaError_t launch_dequantize(const DequantArgs& a, cudaStream_t s);
 cudaError_t launch_group_stats(const StatsArgs& a, cudaStream_t s);
 cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s);

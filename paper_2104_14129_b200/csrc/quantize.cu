@@ -41,6 +41,9 @@ namespace {
 #ifndef ACTNN_NO_WS
 #define ACTNN_NO_WS 0  // build-time diagnostics: 1 sends the mixed path to this file's kernel
 #endif
+#ifndef ACTNN_SP8
+#define ACTNN_SP8 1  // 0: the fp32 single pass runs this file's 4-group kernel
+#endif
 
 constexpr int kU = 4;
 constexpr int kWarps = 8;
@@ -590,6 +593,9 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t s) {
                       (a.sample_base + a.N) * a.D <= (1ll << 35);
     // mixed path (group stats given): the warp-specialised kernel (quantize_ws.cu)
     if (!stats && a.fast && fits && !ACTNN_NO_WS) return launch_quantize_ws(a, s);
+    // fp32 single pass (uniform widths, statistics in-kernel): 8-group units
+    // (quantize_sp8.cu)
+    if (stats && a.fast && fits && a.dt == 0 && ACTNN_SP8) return launch_quantize_sp8(a, s);
     if (a.dt == 0) return stats ? run<float, true>(a, s) : run<float, false>(a, s);
     return stats ? run<uint16_t, true>(a, s) : run<uint16_t, false>(a, s);
 }

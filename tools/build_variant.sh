@@ -10,7 +10,7 @@ NV=/usr/local/cuda/bin/nvcc
 A="-gencode arch=compute_100a,code=sm_100a"
 D=build/var_$TAG
 mkdir -p $D
-for f in abi quantize quantize_ws dequantize stats allocate contexts adapt; do
+for f in abi quantize quantize_ws quantize_sp8 dequantize stats allocate contexts adapt; do
   $NV -O3 -std=c++17 $A -lineinfo -fmad=false -Xcompiler -fPIC,-O2 -Xptxas -v $FLAGS -c $f.cu -o $D/$f.o 2> $D/$f.ptxas.txt &
 done
 wait

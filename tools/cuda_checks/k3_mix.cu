@@ -95,6 +95,36 @@ MIX(m_wide_iadd, wide(a[i], b[i]); iadd(b[i], a[i]);)
 MIX(m_lop_ffma, lop(a[i], b[i]); ffma_imm(f[i], g[i]);)
 MIX(m_lop_fhadd, lop(a[i], b[i]); fhadd(f[i], b[i]);)
 
+// warp-specialised mix: even warps run an IMAD.WIDE stream, odd warps an ALU + FP
+// stream (LOP3 + 2 FFMA) -- do the two overlap when they come from different warps?
+__global__ void m_split(uint32_t iters, uint32_t seed, uint32_t* out) {
+    uint32_t a[CH], b[CH];
+    float f[CH], g[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+        a[i] = threadIdx.x * 7919u + i * 104729u + seed;
+        b[i] = a[i] ^ 0x9E3779B9u;
+        f[i] = (float)(a[i] & 1023) * 0.37f;
+        g[i] = (float)(b[i] & 511) * 0.11f;
+    }
+    if ((threadIdx.x >> 5) & 1) {
+        for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < CH; ++i) { lop(a[i], b[i]); ffma_imm(f[i], g[i]); ffma_imm(g[i], f[i]); }
+        }
+    } else {
+        for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < CH; ++i) { wide(a[i], b[i]); }
+        }
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) acc ^= a[i] ^ b[i] ^ __float_as_uint(f[i]) ^ __float_as_uint(g[i]);
+    if (acc == 0x1234567u) out[0] = acc;
+}
+MIX(m_lop_2ffma, lop(a[i], b[i]); ffma_imm(f[i], g[i]); ffma_imm(g[i], f[i]);)
+
 // ---- the K3 bf16 b = 1 consumer body (one group per lane-iteration)
 struct P {
     RoundKeys rk;
@@ -211,6 +241,7 @@ int main() {
         T(m_wide_ffma2x) T(m_wide_fhadd) T(m_wide_iadd) T(m_lop_ffma) T(m_lop_fhadd)
         T(m_ffma2) T(m_wide_ffma2) T(m_imadlo) T(m_imadhi) T(m_wide_lop1)
         T(m_hilo) T(m_hilo_lop) T(m_hionly) T(m_hionly_lop) T(m_imadlo_lop) T(m_wide_2ffma_lop)
+        T(m_lop_2ffma) T(m_split)
         P pp;
         pp.rk = make_round_keys(42);
         const uint32_t groups = 512;

@@ -11,6 +11,9 @@ SEL_C='relu_pack_and_backward and 1023 or maxpool_forward_backward'
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   extra=""
   [ "$tool" = "racecheck" ] && extra="--racecheck-report hazard"
+  # the fp32 single pass holds 24 mbarriers per CTA (8 warps x 3 stages): above
+  # synccheck's default tracking limit, which then aborts the kernel
+  [ "$tool" = "synccheck" ] && extra="--num-cuda-barriers 128"
   {
     echo "## $tool"
     timeout 1500 $CS --tool $tool $extra --print-limit 400 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_parity.py -k "$SEL_Q" > gpurun_out/sanitize_${tool}_q_full.log 2>&1
