@@ -187,8 +187,28 @@ __device__ __forceinline__ void bulk_wait_all() {
 
 // One group: the lane's 8 codes -> 8 outputs, one vector store (kSh: into the
 // shared staging buffer instead of global memory).
+// b = 1 (bf16 outputs): every code is 0 or 1, so the group has two possible outputs,
+// fmaf(0, scale, Z) and fmaf(1, scale, Z) (the same single-rounding fma as
+// O10, computed once per group); each element selects one by its bit (a
+// predicate test + select instead of unpack, int->float and fma).
+#ifndef ACTNN_DQ_SEL1
+#define ACTNN_DQ_SEL1 1
+#endif
 template <typename TO, int b, bool kSh = false>
 __device__ __forceinline__ void dequant_group(uint64_t pay, float Z, float s, TO* dst) {
+    if constexpr (b == 1 && ACTNN_DQ_SEL1 && sizeof(TO) == 2) {  // bf16 outputs: -1.5% (C4);
+                                                                 // fp32 outputs: no gain
+        const float v0 = __fmaf_rn(0.0f, s, Z), v1 = __fmaf_rn(1.0f, s, Z);
+        const uint32_t p8 = (uint32_t)pay;
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = (p8 & (1u << j)) ? v1 : v0;
+        if constexpr (kSh)
+            sts8(dst, o);
+        else
+            store8(dst, o);
+        return;
+    }
     const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
     const float2 zz = make_float2(Z, Z), ss = make_float2(s, s);
     float o[8];
@@ -244,7 +264,10 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
     TO* stg = reinterpret_cast<TO*>(smem + stg_off<kTS>()) + (size_t)(threadIdx.x >> 5) * kO * kU * kG;
     uint32_t ounit = 0;  // units this warp has staged (kTS)
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
+    // warp index through a shuffle from lane 0: ptxas then knows it (and the
+    // unit walk derived from it) is warp-uniform, keeps the TMA operands in
+    // uniform registers and issues each bulk copy without an ELECT loop
+    const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     uint8_t* ring = smem + (size_t)w * kS * kStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kW * kS * kStage) + w * kS;
     uint8_t* s_bits = smem + (size_t)kW * kS * kStage + (size_t)kW * kS * 8;
@@ -305,12 +328,10 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
     uint32_t pn = gw / p.nb, pj = gw % p.nb;
     uint32_t n = pn, j = pj;
 #ifndef ACTNN_DQ_STOREONLY
-    if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < kS; ++s) {
-            if (pn < p.N) issue(pn, pj, s);
-            advance(pn, pj);
-        }
+    for (int s = 0; s < kS; ++s) {
+        if (lane == 0 && pn < p.N) issue(pn, pj, s);
+        advance(pn, pj);  // every lane: the cursor stays warp-uniform
     }
 #endif
     int stage = 0;
@@ -399,8 +420,8 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
         if (lane == 0) {
             if constexpr (kTS) bulk_s2g(dst, ob, (uint32_t)(gcount * kG * (int)sizeof(TO)));
             if (pn < p.N) issue(pn, pj, stage);
-            advance(pn, pj);
         }
+        advance(pn, pj);
         if constexpr (kTS) ++ounit;  // every lane: they all index the staging ring
         if (++stage == kS) {
             stage = 0;
