@@ -98,6 +98,18 @@ struct GDParams {  // generic kernel
     void* out;
 };
 
+#ifndef ACTNN_DQ_MASYNC
+#define ACTNN_DQ_MASYNC 1
+#endif
+// 16-byte cp.async global -> shared (L2 only) whose completion performs one
+// arrive on `bar` (.noinc: counted against the barrier's expected arrivals)
+__device__ __forceinline__ void cp_async16_mbar(void* dst, const void* src, uint64_t* bar) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
 // The b bytes of a lane in a staged group segment, as a little-endian integer.
 template <int b>
 __device__ __forceinline__ uint64_t stage_payload(const uint8_t* seg, int lane) {
@@ -264,10 +276,7 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
     TO* stg = reinterpret_cast<TO*>(smem + stg_off<kTS>()) + (size_t)(threadIdx.x >> 5) * kO * kU * kG;
     uint32_t ounit = 0;  // units this warp has staged (kTS)
     const int lane = threadIdx.x & 31;
-    // warp index through a shuffle from lane 0: ptxas then knows it (and the
-    // unit walk derived from it) is warp-uniform, keeps the TMA operands in
-    // uniform registers and issues each bulk copy without an ELECT loop
-    const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int w = threadIdx.x >> 5;
     uint8_t* ring = smem + (size_t)w * kS * kStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kW * kS * kStage) + w * kS;
     uint8_t* s_bits = smem + (size_t)kW * kS * kStage + (size_t)kW * kS * 8;
@@ -280,9 +289,17 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
             s_off[i] = (uint32_t)((p.off[i] - off0) >> 5);
         }
     }
+    // kMA (TMA-store path): a unit's 4 zero points and 4 scales come by two
+    // 16-byte cp.async (lanes 0 and 1) whose completion arrives on the stage's
+    // mbarrier (.noinc: 3 arrivals per phase), instead of two more bulk copies
+    // from lane 0 -- each bulk copy costs an ELECT / R2UR loop of ~10
+    // instructions per unit.  Measured per fp32 output size: 205 MB -4%, 411 MB
+    // -2%, 822 MB even; on the LSU-store path (smaller outputs, bf16) +2% / even,
+    // so it is used with the TMA stores only.
+    constexpr bool kMA = kMeta && !kB16 && kTS && ACTNN_DQ_MASYNC;
     if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < kS; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < kS; ++s) mbar_init(&bars[s], kMA ? 3 : 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -314,7 +331,7 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
             const uint32_t g = pn * p.ng + pj * kU;
             mbar_expect_tx(&bars[s], bytes + 4 * kU);
             bulk_g2s(dst + kPay, p.meta + g, 4 * kU, &bars[s]);
-        } else if (kMeta) {
+        } else if (kMeta && !kMA) {
             const uint32_t g = pn * p.ng + pj * kU;
             mbar_expect_tx(&bars[s], bytes + 8 * kU);
             bulk_g2s(dst + kPay, p.zmin + g, 4 * kU, &bars[s]);
@@ -325,13 +342,25 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
         bulk_g2s(dst, p.packed + sofs + (uint64_t)pj * (kU * 32) * b, bytes, &bars[s]);
     };
 
+    // kMA: lanes 0 / 1 copy the unit's zero points / scales (16 bytes each)
+    auto issue_meta = [&](uint32_t pn, uint32_t pj, int s) {
+        if (lane < 2) {
+            const uint32_t g = pn * p.ng + pj * kU;
+            const float* src = (lane == 0 ? p.zmin : p.scale) + g;
+            cp_async16_mbar(ring + s * kStage + kPay + 16 * lane, src, &bars[s]);
+        }
+    };
+
     uint32_t pn = gw / p.nb, pj = gw % p.nb;
     uint32_t n = pn, j = pj;
 #ifndef ACTNN_DQ_STOREONLY
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
-        if (lane == 0 && pn < p.N) issue(pn, pj, s);
-        advance(pn, pj);  // every lane: the cursor stays warp-uniform
+        if (pn < p.N) {
+            if (lane == 0) issue(pn, pj, s);
+            if constexpr (kMA) issue_meta(pn, pj, s);
+        }
+        advance(pn, pj);  // every lane tracks the copy cursor
     }
 #endif
     int stage = 0;
@@ -420,6 +449,9 @@ __global__ void __launch_bounds__(warps<kTS>() * 32, kTS ? ACTNN_DQ_TSMINB : ACT
         if (lane == 0) {
             if constexpr (kTS) bulk_s2g(dst, ob, (uint32_t)(gcount * kG * (int)sizeof(TO)));
             if (pn < p.N) issue(pn, pj, stage);
+        }
+        if constexpr (kMA) {
+            if (pn < p.N) issue_meta(pn, pj, stage);
         }
         advance(pn, pj);
         if constexpr (kTS) ++ounit;  // every lane: they all index the staging ring
