@@ -465,6 +465,10 @@ class Run:
             kseq["quantize"] += ev[2].elapsed_time(ev[3])
             kseq["dequantize"] += ev[3].elapsed_time(ev[4])
         self.kt_seq = {k: v / kb for k, v in kseq.items()}
+        # K2 (+ the exchange when k > 1) of every tensor back to back: latency-bound
+        # single-CTA kernel, reported per launch (<= ~10 us)
+        self.k2_seq_ms = (sum(ev[1].elapsed_time(ev[2]) for ev in seqs) / kb
+                          if plan.mixed else None)
         kt = {"stats": 0.0, "quantize": 0.0, "dequantize": 0.0}
         tq = {"compress": 0.0, "decompress": 0.0}
         for per in evs:
@@ -535,6 +539,13 @@ class Run:
                                "frac_event_pairs": (alg[k] / (kev[k] * 1e-3) / 1e9 / peak)
                                if kev[k] else None}
                            for k in kt}}
+        k2 = getattr(self, "k2_seq_ms", None)
+        if k2:
+            roofline["per_kernel"]["allocate"] = {
+                "kernel": "allocate_kernel (K2)" + (" + all-gather of S" if plan.gather else ""),
+                "bound": "latency (one CTA; overlapped with K1 / K3 of other tensors in the step)",
+                "ms_per_step": k2, "us_per_launch": k2 * 1e3 / nl,
+                "samples_per_launch": plan.layers[0].S.numel()}
         total_alg = sum(alg.values())
         avg_bits = [float(b.double().mean()) for b in bits_host]
         E = world * self.E_loc * self.s_in
@@ -812,6 +823,8 @@ def main():
         line["adapt"] = adapt
     if contexts is not None:
         line["contexts"] = contexts
+    if world == 1 and plan.mixed and not args.no_adapt:
+        line["allocator_latency"] = run_k2_latency(A, max(L.D for L in plan.layers), dev, torch)
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
         allc = oracle_phases(wl, torch, cores, args.cpu_seconds * 0.6)
@@ -955,6 +968,42 @@ def run_adapt(A, plan, xs, wl, s_in, torch, peak, barrier, reps=5):
                        "b_total": b_total, "bits_used": used},
             "note": "NEXT-3 (P:553-569) side measurement, not part of the step; the "
                     "activations stand in for same-shaped gradients"}
+
+
+def run_k2_latency(A, D, dev, torch, reps=50):
+    """K2 (actnn_allocate_bits) alone at batch sizes N = 256 .. 16384 on seeded
+    log-normal sensitivities (avg 2 bits over {1, 2, 4, 8}): per-launch time of
+    `reps` back-to-back launches, and one launch after an idle gap (event pair
+    included).  SURVEY §6 item 5 wants <= ~10 us at N = 4096."""
+    out = {}
+    cs = torch.cuda.current_stream()
+    g = torch.Generator(device="cpu").manual_seed(20260)
+    for N in (256, 1024, 4096, 16384):
+        S = torch.exp(2.0 * torch.randn(N, generator=g, dtype=torch.float64)).to(dev)
+        budget = 2 * N
+        A.allocate_bits(S, budget, D)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)
+        a.record(cs)
+        for _ in range(reps):
+            A.allocate_bits(S, budget, D)
+        b.record(cs)
+        b.synchronize()
+        seq = a.elapsed_time(b) / reps
+        one = 1e9
+        for _ in range(5):
+            torch.cuda._sleep(2_000_000)
+            a.record(cs)
+            A.allocate_bits(S, budget, D)
+            b.record(cs)
+            b.synchronize()
+            one = min(one, a.elapsed_time(b))
+        out[str(N)] = {"us_back_to_back": round(seq * 1e3, 2), "us_single": round(one * 1e3, 2)}
+    return {"kernel": "allocate_kernel (K2)", "D": D, "levels": "{1,2,4,8}", "avg_bits": 2,
+            "by_N": out,
+            "note": "us_back_to_back includes the allocation of the (bits, off) outputs by the "
+                    "Python wrapper (caching allocator); us_single includes one event pair"}
 
 
 def run_e2e(args, plan, xs, outs, out_dt, sp, stream, world, local, dev, torch, dist, s_in,

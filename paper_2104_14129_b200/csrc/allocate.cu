@@ -19,13 +19,18 @@
 //   4. each sample counts its applied moves -> bits[n]; a block scan of
 //      per-thread contiguous sample ranges gives the byte offsets off[N+1].
 // Results are identical to the oracle's heap (tests/test_gpu_parity.py).
+#include <type_traits>
+
 #include "device.cuh"
 #include "launch.h"
 
 namespace actnn {
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef ACTNN_K2_THREADS
+#define ACTNN_K2_THREADS 512
+#endif
+constexpr int kThreads = ACTNN_K2_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kDigit = 11;
 constexpr int kBins = 1 << kDigit;
@@ -46,12 +51,28 @@ struct AParams {
     int64_t* off;
 };
 
-__device__ __forceinline__ uint64_t key_bits(const AParams& p, int64_t n, int c) {
+// w_n = S_n (times gscale_n when given), the weight of sample n's moves
+__device__ __forceinline__ double sample_weight(const AParams& p, int64_t n) {
     double w = __ldg(p.sens + n);
     if (p.gscale) w = __dmul_rn(w, __ldg(p.gscale + n));
+    return w;
+}
+// key of move c of sample n = RN(w_n * slope_c), as its bit pattern.
+__device__ __forceinline__ uint64_t key_of(const AParams& p, double w, int c) {
     const double k = __dmul_rn(w, p.slope[c]);
     return k == 0.0 ? 0ull : (uint64_t)__double_as_longlong(k);  // -0 orders as +0
 }
+
+// Where the sweeps over all moves read their keys (K2 sweeps over every move
+// 4-6 times: min/max, 2-3 radix passes, the candidate compaction, the widths):
+//   kCache 2: the N*M keys were computed once into shared memory (key_s,
+//             move (n, c) at c*N + n) -- N*M <= 24576;
+//   kCache 1: the N weights w_n are in shared memory, keys recomputed;
+//   kCache 0: everything from global memory (L2), 64-bit indices.
+// With a cache the loops also run on 32-bit indices: at N = 4096 (M = 3) the
+// kernel was instruction-bound on 64-bit index / key arithmetic (ncu: 88k
+// warp-instructions, ISETP / IMAD / SEL on top, no memory stalls).
+constexpr size_t kCacheBytes = 24576 * sizeof(uint64_t);
 
 struct Shared {
     int whist[kBins];
@@ -96,12 +117,69 @@ __device__ __forceinline__ long long block_excl_scan(long long v, Shared& sh, lo
     return res;
 }
 
+// Diagnostics (-DACTNN_K2_PROF, tools/k2_phases.py): thread 0's clock64 at the
+// phase boundaries, written over off[1..] at the end (off[0] = -count).
+#ifdef ACTNN_K2_PROF
+#define K2_MARK_INIT() long long T_[16]; int nt_ = 0; T_[nt_++] = clock64()
+#define K2_MARK() do { if (nt_ < 16) T_[nt_++] = clock64(); } while (0)
+#define K2_DUMP() do { K2_MARK(); __syncthreads(); if (tid == 0) { \
+    for (int i_ = 1; i_ < nt_; ++i_) p.off[i_] = T_[i_] - T_[0]; p.off[0] = -nt_; } } while (0)
+#else
+#define K2_MARK_INIT() do {} while (0)
+#define K2_MARK() do {} while (0)
+#define K2_DUMP() do {} while (0)
+#endif
+
+template <int kCache>
 __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
     pdl_trigger();  // the next kernel of the stream may start launching
     pdl_wait();     // the previous grid is complete and visible
+    K2_MARK_INIT();
+    using Idx = typename std::conditional<kCache != 0, int, int64_t>::type;
     __shared__ Shared sh;
+    extern __shared__ uint64_t cache_s[];  // kCache 2: keys; 1: weights (as doubles)
+    double* w_s = reinterpret_cast<double*>(cache_s);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const Idx N = (Idx)p.N;
+    if (kCache == 1) {
+        for (Idx n = tid; n < N; n += kThreads) w_s[n] = sample_weight(p, n);
+        __syncthreads();
+    }
+    // kCache 2: the keys are computed once (4 samples in flight per thread) and
+    // their min / max taken on the way
+    unsigned long long lmin = ~0ull, lmax = 0ull;
+    if (kCache == 2) {
+        // batches of 8 samples per thread: their global loads are all in flight
+        // before the first key is formed
+        for (Idx n0 = tid; n0 < N; n0 += 8 * kThreads) {
+            double w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const Idx n = n0 + i * kThreads;
+                w[i] = n < N ? sample_weight(p, n) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const Idx n = n0 + i * kThreads;
+                if (n < N) {
+                    for (int c = 0; c < p.M; ++c) {
+                        const uint64_t k = key_of(p, w[i], c);
+                        cache_s[(Idx)c * N + n] = k;
+                        lmin = min(lmin, (unsigned long long)k);
+                        lmax = max(lmax, (unsigned long long)k);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    auto key_bits = [&](const AParams& q, Idx n, int c) -> uint64_t {
+        if (kCache == 2) return cache_s[(Idx)c * N + n];
+        if (kCache == 1) return key_of(q, w_s[n], c);
+        return key_of(q, sample_weight(q, n), c);
+    };
     const int M = p.M;
+    K2_MARK();
     const int64_t total_moves = p.N * (int64_t)M;
     const bool any = (p.need > 0 && M > 0);
     uint64_t key_star = 0;
@@ -109,9 +187,8 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
 
     if (any) {
         // ---- 1. min / max key
-        unsigned long long lmin = ~0ull, lmax = 0ull;
-        for (int c = 0; c < M; ++c)
-            for (int64_t n = tid; n < p.N; n += kThreads) {
+        for (int c = 0; c < (kCache == 2 ? 0 : M); ++c)
+            for (Idx n = tid; n < N; n += kThreads) {
                 const uint64_t k = key_bits(p, n, c);
                 lmin = min(lmin, (unsigned long long)k);
                 lmax = max(lmax, (unsigned long long)k);
@@ -133,6 +210,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             kmax = max(kmax, sh.kmax[w]);
         }
         // ---- 2. weighted radix select below the common prefix
+        K2_MARK();
         uint64_t prefix, pmask;
         long long rem = p.need;
         long long count = total_moves;  // moves matching the prefix
@@ -156,10 +234,11 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             }
             __syncthreads();
             for (int c = 0; c < M; ++c) {
-                for (int64_t base = 0; base < p.N; base += kThreads) {
-                    const int64_t n = base + tid;
+#pragma unroll 4
+                for (Idx base = 0; base < N; base += kThreads) {
+                    const Idx n = base + tid;
                     int digit = kBins;  // sentinel: not a candidate
-                    if (n < p.N) {
+                    if (n < N) {
                         const uint64_t k = key_bits(p, n, c);
                         if (((k ^ prefix) & pmask) == 0) digit = (int)((k >> shift) & dmask);
                     }
@@ -196,6 +275,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             rem -= sh.dbefore;
             count = sh.dcount;
             hi = shift - 1;
+            K2_MARK();
             __syncthreads();  // sh.digit / dbefore / dcount are rewritten next pass
         }
         if (count <= 32) {
@@ -203,7 +283,8 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             if (tid == 0) sh.ncand = 0;
             __syncthreads();
             for (int c = 0; c < M; ++c)
-                for (int64_t n = tid; n < p.N; n += kThreads) {
+#pragma unroll 4
+                for (Idx n = tid; n < N; n += kThreads) {
                     const uint64_t k = key_bits(p, n, c);
                     if (((k ^ prefix) & pmask) == 0) {
                         const int slot = atomicAdd(&sh.ncand, 1);
@@ -264,7 +345,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                 const int64_t mv = base + tid;
                 int xv = 0;
                 if (mv < total_moves) {
-                    const int64_t n = mv / M;
+                    const Idx n = (Idx)(mv / M);
                     const int c = (int)(mv - n * M);
                     if (key_bits(p, n, c) == key_star) xv = p.freed[c];
                 }
@@ -283,9 +364,10 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
     }
 
     // ---- 4. widths and byte offsets (thread t: a contiguous range of samples)
-    const int64_t per = (p.N + kThreads - 1) / kThreads;
-    const int64_t n0 = min(p.N, (int64_t)tid * per), n1 = min(p.N, n0 + per);
-    auto width = [&](int64_t n) {  // bits of sample n: its applied moves
+    K2_MARK();
+    const Idx per = (N + kThreads - 1) / kThreads;
+    const Idx n0 = min(N, (Idx)tid * per), n1 = min(N, n0 + per);
+    auto width = [&](Idx n) {  // bits of sample n: its applied moves
         int cnt = 0;
         if (any) {
             for (int c = 0; c < M; ++c) {
@@ -296,17 +378,41 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
         }
         return p.L[cnt];
     };
-    long long local = 0;
-    for (int64_t n = n0; n < n1; ++n) local += (long long)width(n) * p.unit;
     long long tot;
+    if (kCache != 0 && (size_t)N <= sizeof(sh.whist)) {
+        // the widths computed once, coalesced, into the (now idle) histogram
+        // space; the per-thread ranges then read bytes instead of M keys each
+        uint8_t* wb = reinterpret_cast<uint8_t*>(sh.whist);
+        __syncthreads();
+#pragma unroll 4
+        for (Idx n = tid; n < N; n += kThreads) wb[n] = (uint8_t)width(n);
+        __syncthreads();
+        long long local = 0;
+        for (Idx n = n0; n < n1; ++n) local += wb[n];
+        K2_MARK();
+        long long run = block_excl_scan(local * p.unit, sh, &tot);
+        if (tid == 0) p.off[0] = 0;
+        for (Idx n = n0; n < n1; ++n) {
+            const int b = wb[n];
+            p.bits[n] = (uint8_t)b;
+            run += (long long)b * p.unit;
+            p.off[n + 1] = run;
+        }
+        K2_DUMP();
+        return;
+    }
+    long long local = 0;
+    for (Idx n = n0; n < n1; ++n) local += (long long)width(n) * p.unit;
+    K2_MARK();
     long long run = block_excl_scan(local, sh, &tot);
     if (tid == 0) p.off[0] = 0;
-    for (int64_t n = n0; n < n1; ++n) {  // recomputed: no read-back of global writes
+    for (Idx n = n0; n < n1; ++n) {  // recomputed: no read-back of global writes
         const int b = width(n);
         p.bits[n] = (uint8_t)b;
         run += (long long)b * p.unit;
         p.off[n + 1] = run;
     }
+    K2_DUMP();
 }
 
 __global__ void uniform_bits_kernel(int64_t N, int b, int64_t unit, uint8_t* bits, int64_t* off) {
@@ -335,7 +441,17 @@ cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s) {
     p.unit = a.unit;
     p.bits = a.bits;
     p.off = a.off;
-    launch_pdl(allocate_kernel, 1, kThreads, 0, s, p);
+    // keys (N*M <= 24576) or weights (N <= 24576) staged in shared memory
+    const int64_t nm = a.N * (int64_t)p.M;
+    if (a.N > 0 && nm > 0 && nm * (int64_t)sizeof(uint64_t) <= (int64_t)kCacheBytes) {
+        ensure_smem_attr((const void*)allocate_kernel<2>, kCacheBytes);
+        launch_pdl(allocate_kernel<2>, 1, kThreads, (size_t)nm * sizeof(uint64_t), s, p);
+    } else if (a.N > 0 && a.N * (int64_t)sizeof(double) <= (int64_t)kCacheBytes) {
+        ensure_smem_attr((const void*)allocate_kernel<1>, kCacheBytes);
+        launch_pdl(allocate_kernel<1>, 1, kThreads, (size_t)a.N * sizeof(double), s, p);
+    } else {
+        launch_pdl(allocate_kernel<0>, 1, kThreads, 0, s, p);
+    }
     return cudaGetLastError();
 }
 

@@ -195,6 +195,11 @@ def _w_cases(rng):
     yield "ties", w
     yield "n4096", np.exp(rng.standard_normal(4096))
     yield "n20000", np.exp(3 * rng.standard_normal(20000))
+    # K2 stages the sample weights in shared memory up to 24576 samples; above
+    # that it reads them from global memory (both kernels, both tie paths)
+    yield "n24576", np.exp(rng.standard_normal(24576))
+    yield "n30000", np.exp(3 * rng.standard_normal(30000))
+    yield "equal_n30000", np.ones(30000)
     yield "single", np.array([3.0])
 
 
