@@ -1,0 +1,8 @@
+#!/bin/bash
+V=paper_2104_14129_b200/csrc/build
+for rep in 1 2; do for v in default wst1; do
+  L=paper_2104_14129_b200/libactnn.so; [ $v != default ] && L=$V/var_$v/libactnn.so
+  timeout 600 python tools/with_variant.py $L -- bench.py --config c2 --no-cpu --no-e2e --no-adapt > gpurun_out/s62_${v}_$rep.log 2>&1
+  echo "$v $rep $(python tools/bl.py gpurun_out/s62_${v}_$rep.log)"
+done; done
+timeout 900 python tools/with_variant.py $V/var_wst2/libactnn.so -- -m pytest tests/test_gpu_parity.py tests/test_gpu_full_parity.py -q -x -k "c1 or adversarial or ragged or c2 or multi_tile or philox or uncached" 2>&1 | tail -1
