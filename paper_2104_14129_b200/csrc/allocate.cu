@@ -73,6 +73,7 @@ __device__ __forceinline__ uint64_t key_of(const AParams& p, double w, int c) {
 // kernel was instruction-bound on 64-bit index / key arithmetic (ncu: 88k
 // warp-instructions, ISETP / IMAD / SEL on top, no memory stalls).
 constexpr size_t kCacheBytes = 24576 * sizeof(uint64_t);
+constexpr int64_t kCacheMinN = 1024;
 
 struct Shared {
     int whist[kBins];
@@ -441,12 +442,16 @@ cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s) {
     p.unit = a.unit;
     p.bits = a.bits;
     p.off = a.off;
-    // keys (N*M <= 24576) or weights (N <= 24576) staged in shared memory
+    // keys (N*M <= 24576) or weights (N <= 24576) staged in shared memory from
+    // N = 1024 on; below, the sweeps' L2 reads cost no more (measured warm), and
+    // launched cold (ncu's serialised list) the staging pass costs ~3 us at N = 256
     const int64_t nm = a.N * (int64_t)p.M;
-    if (a.N > 0 && nm > 0 && nm * (int64_t)sizeof(uint64_t) <= (int64_t)kCacheBytes) {
+    if (a.N < kCacheMinN) {
+        launch_pdl(allocate_kernel<0>, 1, kThreads, 0, s, p);
+    } else if (nm > 0 && nm * (int64_t)sizeof(uint64_t) <= (int64_t)kCacheBytes) {
         ensure_smem_attr((const void*)allocate_kernel<2>, kCacheBytes);
         launch_pdl(allocate_kernel<2>, 1, kThreads, (size_t)nm * sizeof(uint64_t), s, p);
-    } else if (a.N > 0 && a.N * (int64_t)sizeof(double) <= (int64_t)kCacheBytes) {
+    } else if (a.N * (int64_t)sizeof(double) <= (int64_t)kCacheBytes) {
         ensure_smem_attr((const void*)allocate_kernel<1>, kCacheBytes);
         launch_pdl(allocate_kernel<1>, 1, kThreads, (size_t)a.N * sizeof(double), s, p);
     } else {

@@ -193,6 +193,8 @@ def _w_cases(rng):
     w = np.exp(rng.standard_normal(512))
     w[::3] = w[0]                              # many exact ties across samples
     yield "ties", w
+    yield "n1023", np.exp(2.0 * rng.standard_normal(1023))   # K2 from global memory
+    yield "n1024", np.exp(2.0 * rng.standard_normal(1024))   # K2 keys in shared memory
     yield "n4096", np.exp(rng.standard_normal(4096))
     yield "n20000", np.exp(3 * rng.standard_normal(20000))
     # K2 stages the sample weights in shared memory up to 24576 samples; above
