@@ -27,6 +27,9 @@
 namespace actnn {
 namespace {
 
+#ifndef ACTNN_K2_NOMATCH
+#define ACTNN_K2_NOMATCH 1  // kCache 2: per-lane packed atomics (match.any: N = 4096 23.7 -> 19.1 us)
+#endif
 #ifndef ACTNN_K2_THREADS
 #define ACTNN_K2_THREADS 512
 #endif
@@ -59,7 +62,11 @@ __device__ __forceinline__ double sample_weight(const AParams& p, int64_t n) {
 }
 // key of move c of sample n = RN(w_n * slope_c), as its bit pattern.
 __device__ __forceinline__ uint64_t key_of(const AParams& p, double w, int c) {
+#ifdef ACTNN_K2_DIAG_NODMUL  // diagnostics only (wrong keys): the cost of the fp64 multiply
+    const double k = w;
+#else
     const double k = __dmul_rn(w, p.slope[c]);
+#endif
     return k == 0.0 ? 0ull : (uint64_t)__double_as_longlong(k);  // -0 orders as +0
 }
 
@@ -73,6 +80,9 @@ __device__ __forceinline__ uint64_t key_of(const AParams& p, double w, int c) {
 // kernel was instruction-bound on 64-bit index / key arithmetic (ncu: 88k
 // warp-instructions, ISETP / IMAD / SEL on top, no memory stalls).
 constexpr size_t kCacheBytes = 24576 * sizeof(uint64_t);
+// kCache 2 holds at most 16383 keys: a bin's freed-bit sum (<= 7 per move) and
+// move count then share one 32-bit histogram word (17 + 14 bits)
+constexpr int64_t kKeyCap = 16383;
 constexpr int64_t kCacheMinN = 1024;
 
 struct Shared {
@@ -84,6 +94,7 @@ struct Shared {
     long long cand_mv[32];
     int cand_freed[32];
     int ncand;
+    int L[8];  // width after c applied moves (per-lane divergent lookups: shared, not the param bank)
     int digit, dcount;
     long long dbefore;
     unsigned long long keystar;
@@ -142,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
     double* w_s = reinterpret_cast<double*>(cache_s);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const Idx N = (Idx)p.N;
+    if (tid < 8) sh.L[tid] = p.L[tid];  // visible after the first __syncthreads below
     if (kCache == 1) {
         for (Idx n = tid; n < N; n += kThreads) w_s[n] = sample_weight(p, n);
         __syncthreads();
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             const uint64_t dmask = (width == 64) ? ~0ull : ((1ull << width) - 1ull);
             for (int i = tid; i < kBins; i += kThreads) {
                 sh.whist[i] = 0;
-                sh.chist[i] = 0;
+                if (kCache != 2) sh.chist[i] = 0;
             }
             __syncthreads();
             for (int c = 0; c < M; ++c) {
@@ -243,31 +255,47 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                         const uint64_t k = key_bits(p, n, c);
                         if (((k ^ prefix) & pmask) == 0) digit = (int)((k >> shift) & dmask);
                     }
+#if ACTNN_K2_NOMATCH
+                    if (kCache == 2) {  // every lane its own atomic, no match.any
+                        if (digit < kBins) atomicAdd(&sh.whist[digit], (p.freed[c] << 14) | 1);
+                        continue;
+                    }
+#endif
                     const unsigned peers = __match_any_sync(kFull, digit);
                     if (digit < kBins && lane == __ffs(peers) - 1) {
-                        atomicAdd(&sh.whist[digit], __popc(peers) * p.freed[c]);
-                        atomicAdd(&sh.chist[digit], __popc(peers));
+                        if (kCache == 2) {  // freed-bit sum << 14 | move count, one atomic
+                            atomicAdd(&sh.whist[digit], __popc(peers) * ((p.freed[c] << 14) | 1));
+                        } else {
+                            atomicAdd(&sh.whist[digit], __popc(peers) * p.freed[c]);
+                            atomicAdd(&sh.chist[digit], __popc(peers));
+                        }
                     }
                 }
             }
             __syncthreads();
             // scan the bins: thread t owns bins [t*K, t*K + K)
+            auto bin_w = [&](int bin) -> int {
+                return kCache == 2 ? (int)((unsigned)sh.whist[bin] >> 14) : sh.whist[bin];
+            };
+            auto bin_c = [&](int bin) -> int {
+                return kCache == 2 ? (sh.whist[bin] & 0x3FFF) : sh.chist[bin];
+            };
             long long loc = 0;
 #pragma unroll
-            for (int i = 0; i < kBinsPerThread; ++i) loc += sh.whist[tid * kBinsPerThread + i];
+            for (int i = 0; i < kBinsPerThread; ++i) loc += bin_w(tid * kBinsPerThread + i);
             long long tot;
             const long long excl = block_excl_scan(loc, sh, &tot);
             if (excl < rem && rem <= excl + loc) {
                 long long cum = excl;
                 for (int i = 0; i < kBinsPerThread; ++i) {
                     const int bin = tid * kBinsPerThread + i;
-                    if (cum + sh.whist[bin] >= rem) {
+                    if (cum + bin_w(bin) >= rem) {
                         sh.digit = bin;
                         sh.dbefore = cum;
-                        sh.dcount = sh.chist[bin];
+                        sh.dcount = bin_c(bin);
                         break;
                     }
-                    cum += sh.whist[bin];
+                    cum += bin_w(bin);
                 }
             }
             __syncthreads();
@@ -366,6 +394,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
 
     // ---- 4. widths and byte offsets (thread t: a contiguous range of samples)
     K2_MARK();
+    __syncthreads();  // sh.L (written at entry) is visible even when no move was made
     const Idx per = (N + kThreads - 1) / kThreads;
     const Idx n0 = min(N, (Idx)tid * per), n1 = min(N, n0 + per);
     auto width = [&](Idx n) {  // bits of sample n: its applied moves
@@ -377,27 +406,42 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                 if (k < key_star || (k == key_star && mv <= cut)) ++cnt;
             }
         }
-        return p.L[cnt];
+        return sh.L[cnt];
     };
     long long tot;
     if (kCache != 0 && (size_t)N <= sizeof(sh.whist)) {
         // the widths computed once, coalesced, into the (now idle) histogram
         // space; the per-thread ranges then read bytes instead of M keys each
+        // warp w then owns samples [w CH, (w + 1) CH), lane-interleaved, so the
+        // bits / off stores are coalesced; off = unit * (inclusive bit sums)
         uint8_t* wb = reinterpret_cast<uint8_t*>(sh.whist);
         __syncthreads();
 #pragma unroll 4
         for (Idx n = tid; n < N; n += kThreads) wb[n] = (uint8_t)width(n);
         __syncthreads();
-        long long local = 0;
-        for (Idx n = n0; n < n1; ++n) local += wb[n];
+        const Idx CH = ((N + kWarps - 1) / kWarps + 31) / 32 * 32;
+        const Idx c0 = min(N, (Idx)wid * CH), c1 = min(N, c0 + CH);
+        int wsum = 0;
+        for (Idx n = c0 + lane; n < c1; n += 32) wsum += wb[n];
+        wsum = __reduce_add_sync(kFull, wsum);
         K2_MARK();
-        long long run = block_excl_scan(local * p.unit, sh, &tot);
+        long long run = block_excl_scan(lane == 0 ? (long long)wsum : 0ll, sh, &tot);
+        run = __shfl_sync(kFull, run, 0);  // bits before this warp's chunk
         if (tid == 0) p.off[0] = 0;
-        for (Idx n = n0; n < n1; ++n) {
-            const int b = wb[n];
-            p.bits[n] = (uint8_t)b;
-            run += (long long)b * p.unit;
-            p.off[n + 1] = run;
+        for (Idx base = c0; base < c1; base += 32) {
+            const Idx n = base + lane;
+            const int b = n < c1 ? (int)wb[n] : 0;
+            int incl = b;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (n < c1) {
+                p.bits[n] = (uint8_t)b;
+                p.off[n + 1] = (run + incl) * p.unit;
+            }
+            run += __shfl_sync(kFull, incl, 31);
         }
         K2_DUMP();
         return;
@@ -448,7 +492,7 @@ cudaError_t launch_allocate(const AllocArgs& a, cudaStream_t s) {
     const int64_t nm = a.N * (int64_t)p.M;
     if (a.N < kCacheMinN) {
         launch_pdl(allocate_kernel<0>, 1, kThreads, 0, s, p);
-    } else if (nm > 0 && nm * (int64_t)sizeof(uint64_t) <= (int64_t)kCacheBytes) {
+    } else if (nm > 0 && nm <= kKeyCap) {
         ensure_smem_attr((const void*)allocate_kernel<2>, kCacheBytes);
         launch_pdl(allocate_kernel<2>, 1, kThreads, (size_t)nm * sizeof(uint64_t), s, p);
     } else if (a.N * (int64_t)sizeof(double) <= (int64_t)kCacheBytes) {
