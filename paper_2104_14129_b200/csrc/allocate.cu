@@ -28,7 +28,7 @@ namespace actnn {
 namespace {
 
 #ifndef ACTNN_K2_NOMATCH
-#define ACTNN_K2_NOMATCH 1  // kCache 2: per-lane packed atomics (match.any: N = 4096 23.7 -> 19.1 us)
+#define ACTNN_K2_NOMATCH 1  // packed histogram: per-lane atomics (match.any: N = 4096 23.7 -> 19.1 us)
 #endif
 #ifndef ACTNN_K2_THREADS
 #define ACTNN_K2_THREADS 512
@@ -80,8 +80,8 @@ __device__ __forceinline__ uint64_t key_of(const AParams& p, double w, int c) {
 // kernel was instruction-bound on 64-bit index / key arithmetic (ncu: 88k
 // warp-instructions, ISETP / IMAD / SEL on top, no memory stalls).
 constexpr size_t kCacheBytes = 24576 * sizeof(uint64_t);
-// kCache 2 holds at most 16383 keys: a bin's freed-bit sum (<= 7 per move) and
-// move count then share one 32-bit histogram word (17 + 14 bits)
+// kCache 2 holds at most 16383 keys; up to that many moves a bin's freed-bit sum
+// (<= 7 per move) and move count share one 32-bit histogram word (17 + 14 bits)
 constexpr int64_t kKeyCap = 16383;
 constexpr int64_t kCacheMinN = 1024;
 
@@ -194,6 +194,9 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
     const int M = p.M;
     K2_MARK();
     const int64_t total_moves = p.N * (int64_t)M;
+    // up to kKeyCap moves (every kCache 2 launch, and small batches): a bin's
+    // freed-bit sum and move count share one 32-bit histogram word
+    const bool packed = total_moves <= kKeyCap;
     const bool any = (p.need > 0 && M > 0);
     uint64_t key_star = 0;
     long long cut = -1;
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             const uint64_t dmask = (width == 64) ? ~0ull : ((1ull << width) - 1ull);
             for (int i = tid; i < kBins; i += kThreads) {
                 sh.whist[i] = 0;
-                if (kCache != 2) sh.chist[i] = 0;
+                if (!packed) sh.chist[i] = 0;
             }
             __syncthreads();
             for (int c = 0; c < M; ++c) {
@@ -256,14 +259,14 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                         if (((k ^ prefix) & pmask) == 0) digit = (int)((k >> shift) & dmask);
                     }
 #if ACTNN_K2_NOMATCH
-                    if (kCache == 2) {  // every lane its own atomic, no match.any
+                    if (packed) {  // every lane its own atomic, no match.any
                         if (digit < kBins) atomicAdd(&sh.whist[digit], (p.freed[c] << 14) | 1);
                         continue;
                     }
 #endif
                     const unsigned peers = __match_any_sync(kFull, digit);
                     if (digit < kBins && lane == __ffs(peers) - 1) {
-                        if (kCache == 2) {  // freed-bit sum << 14 | move count, one atomic
+                        if (packed) {  // freed-bit sum << 14 | move count, one atomic
                             atomicAdd(&sh.whist[digit], __popc(peers) * ((p.freed[c] << 14) | 1));
                         } else {
                             atomicAdd(&sh.whist[digit], __popc(peers) * p.freed[c]);
@@ -275,10 +278,10 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
             __syncthreads();
             // scan the bins: thread t owns bins [t*K, t*K + K)
             auto bin_w = [&](int bin) -> int {
-                return kCache == 2 ? (int)((unsigned)sh.whist[bin] >> 14) : sh.whist[bin];
+                return packed ? (int)((unsigned)sh.whist[bin] >> 14) : sh.whist[bin];
             };
             auto bin_c = [&](int bin) -> int {
-                return kCache == 2 ? (sh.whist[bin] & 0x3FFF) : sh.chist[bin];
+                return packed ? (sh.whist[bin] & 0x3FFF) : sh.chist[bin];
             };
             long long loc = 0;
 #pragma unroll
