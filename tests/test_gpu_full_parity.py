@@ -303,3 +303,61 @@ def test_tma_store_dequantize_large_fp32(A, W, N, D):
     if not np.array_equal(got, exp.view(np.uint32)):
         bad = np.argwhere(got != exp.view(np.uint32))
         raise AssertionError(f"{len(bad)} values differ, first {bad[:4].tolist()}")
+
+
+def test_c5_eight_virtual_ranks_plan_path(A, W):
+    """"k-rank == 1-rank plus rank 0's shard".  One
+    C5 tensor (ResNet-152 layer4.1.conv2 input shape, batch 4096, bf16, avg 1.25
+    bits) split over k = 8 virtual ranks of 512 samples, each driven through
+    the product's multi-rank path (ActivationSetPlan with n_total / sample_base
+    and an exchange closure, PipelinedStep) on one GPU.  The closure delivers
+    every rank's S_n (each rank's own slice is checked against what its stats
+    kernel wrote); every rank's widths, packed bytes, zmin / scale and
+    dequantised values must equal the oracle's sharded driver O13 for that rank
+    (P:541-566 global greedy, P:491-508 per-group quantisation)."""
+    from paper_2104_14129_b200.plan import ActivationSetPlan, PipelinedStep
+    wl = W.workload("c5")
+    t = 300
+    act = wl.acts[t]
+    N, k = wl.N, 8
+    n_loc = N // k
+    x = W.synth_activation(act, N, t, "bf16", DEV)
+    S_all = torch.zeros(N, dtype=torch.float64, device=DEV)
+    for r in range(k):
+        A.group_stats(x[r * n_loc:(r + 1) * n_loc], sens_out=S_all[r * n_loc:(r + 1) * n_loc])
+    torch.cuda.synchronize()
+    seed = W.quant_seed(t)
+    got = []
+    for r in range(k):
+        lo, hi = r * n_loc, (r + 1) * n_loc
+
+        def gather(S_global, S_local, lo=lo, hi=hi):
+            assert torch.equal(S_local, S_all[lo:hi]), "rank's own S_n"
+            S_global.copy_(S_all)
+
+        xs = [x[lo:hi].contiguous()]
+        plan = ActivationSetPlan(xs, [seed], avg_bits=1.25, n_total=N, sample_base=lo,
+                                 gather=gather)
+        outs = [torch.empty(xs[0].numel(), dtype=torch.bfloat16, device=DEV)]
+        ps = PipelinedStep(plan, outs, A.api.BF16, DEV)
+        with torch.cuda.stream(ps.stream):
+            ps()
+        torch.cuda.synchronize()
+        L = plan.layers[0]
+        off = host(L.off[lo:hi + 1])
+        got.append((host(L.bits[lo:hi]), host(L.packed[:int(off[-1] - off[0])]),
+                    host(L.zmin).view(np.uint32), host(L.scale).view(np.uint32),
+                    out_bits(outs[0], xs[0].numel())))
+        del plan, ps, outs, xs
+    xh = x_host(x)
+    ref = O.sharded_quantize(xh, k, 1.25, seed, threads=CORES)
+    D = act.D
+    for r in range(k):
+        bits, packed, zmin, scale, out = got[r]
+        rp, rz, rs, rb = ref[r]
+        assert np.array_equal(bits, rb), (r, "bits")
+        assert np.array_equal(packed, rp), (r, "packed")
+        assert np.array_equal(zmin, rz.ravel().view(np.uint32)), (r, "zmin")
+        assert np.array_equal(scale, rs.ravel().view(np.uint32)), (r, "scale")
+        exp = O.dequantize(rp, rz, rs, rb, n_loc, D, out_dtype=O.BF16, threads=CORES)
+        assert np.array_equal(out, exp.ravel()), (r, "dequantised")
