@@ -9,15 +9,18 @@
 //   1. min and max key (non-negative doubles order like their bit patterns);
 //      the bits above their highest differing bit are common to every move;
 //   2. weighted radix select from that bit down, 11-bit digits: a 2048-bin
-//      histogram of freed bits (and of move counts) among the moves matching
-//      the prefix so far, warp-aggregated with match.any, and a block scan
-//      that finds the digit where the cumulative freed bits reach the
-//      remainder; stop as soon as the chosen digit holds <= 32 moves;
+//      histogram of freed bits and of move counts among the moves matching
+//      the prefix so far (up to 16383 moves both in one 32-bit word per bin,
+//      one shared atomic per lane; above, two histograms, warp-aggregated with
+//      match.any), and a block scan that finds the digit where the cumulative
+//      freed bits reach the remainder; stop once the chosen digit holds <= 32
+//      moves;
 //   3. those <= 32 candidates are compacted, sorted by (key, move index) with
 //      a one-warp bitonic network and scanned -> the cut move (if more than 32
 //      moves share one full 64-bit key, a block scan in index order instead);
-//   4. each sample counts its applied moves -> bits[n]; a block scan of
-//      per-thread contiguous sample ranges gives the byte offsets off[N+1].
+//   4. each sample counts its applied moves -> bits[n]; a block scan gives
+//      the byte offsets off[N+1] (staged widths: per-warp contiguous ranges,
+//      lane-interleaved, coalesced stores; else per-thread ranges).
 // Results are identical to the oracle's heap (tests/test_gpu_parity.py).
 #include <type_traits>
 
@@ -72,10 +75,12 @@ __device__ __forceinline__ uint64_t key_of(const AParams& p, double w, int c) {
 
 // Where the sweeps over all moves read their keys (K2 sweeps over every move
 // 4-6 times: min/max, 2-3 radix passes, the candidate compaction, the widths):
-//   kCache 2: the N*M keys were computed once into shared memory (key_s,
-//             move (n, c) at c*N + n) -- N*M <= 24576;
-//   kCache 1: the N weights w_n are in shared memory, keys recomputed;
-//   kCache 0: everything from global memory (L2), 64-bit indices.
+//   kCache 2: the N*M keys were computed once into shared memory (cache_s,
+//             move (n, c) at c*N + n) -- N >= 1024 and N*M <= kKeyCap;
+//   kCache 1: the N weights w_n are in shared memory (N <= 24576), keys
+//             recomputed;
+//   kCache 0: everything from global memory (L2), 64-bit indices (N < 1024
+//             or N > 24576).
 // With a cache the loops also run on 32-bit indices: at N = 4096 (M = 3) the
 // kernel was instruction-bound on 64-bit index / key arithmetic (ncu: 88k
 // warp-instructions, ISETP / IMAD / SEL on top, no memory stalls).
