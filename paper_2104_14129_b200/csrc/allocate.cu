@@ -22,6 +22,7 @@
 //      the byte offsets off[N+1] (staged widths: per-warp contiguous ranges,
 //      lane-interleaved, coalesced stores; else per-thread ranges).
 // Results are identical to the oracle's heap (tests/test_gpu_parity.py).
+#include <cassert>
 #include <type_traits>
 
 #include "device.cuh"
@@ -134,6 +135,15 @@ __device__ __forceinline__ long long block_excl_scan(long long v, Shared& sh, lo
     return res;
 }
 
+// Debug builds (-DACTNN_K2_ASSERT, tools/r02_gpu82.sh): device asserts on every
+// shared-memory index of the staged paths (compute-sanitizer is not available
+// on the pool for the rest of round 2)
+#ifdef ACTNN_K2_ASSERT
+#define K2_ASSERT(c) assert(c)
+#else
+#define K2_ASSERT(c) do {} while (0)
+#endif
+
 // Diagnostics (-DACTNN_K2_PROF, tools/k2_phases.py): thread 0's clock64 at the
 // phase boundaries, written over off[1..] at the end (off[0] = -count).
 #ifdef ACTNN_K2_PROF
@@ -160,7 +170,10 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
     const Idx N = (Idx)p.N;
     if (tid < 8) sh.L[tid] = p.L[tid];  // visible after the first __syncthreads below
     if (kCache == 1) {
-        for (Idx n = tid; n < N; n += kThreads) w_s[n] = sample_weight(p, n);
+        for (Idx n = tid; n < N; n += kThreads) {
+            K2_ASSERT((size_t)(n + 1) * sizeof(double) <= kCacheBytes);
+            w_s[n] = sample_weight(p, n);
+        }
         __syncthreads();
     }
     // kCache 2: the keys are computed once (4 samples in flight per thread) and
@@ -182,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                 if (n < N) {
                     for (int c = 0; c < p.M; ++c) {
                         const uint64_t k = key_of(p, w[i], c);
+                        K2_ASSERT((int64_t)c * N + n < kKeyCap);
                         cache_s[(Idx)c * N + n] = k;
                         lmin = min(lmin, (unsigned long long)k);
                         lmax = max(lmax, (unsigned long long)k);
@@ -325,6 +339,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                     const uint64_t k = key_bits(p, n, c);
                     if (((k ^ prefix) & pmask) == 0) {
                         const int slot = atomicAdd(&sh.ncand, 1);
+                        K2_ASSERT(slot < 32);
                         sh.cand_key[slot] = k;
                         sh.cand_mv[slot] = n * (long long)M + c;
                         sh.cand_freed[slot] = p.freed[c];
@@ -414,6 +429,7 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
                 if (k < key_star || (k == key_star && mv <= cut)) ++cnt;
             }
         }
+        K2_ASSERT(cnt < 8);
         return sh.L[cnt];
     };
     long long tot;
@@ -425,7 +441,10 @@ __global__ void __launch_bounds__(kThreads) allocate_kernel(AParams p) {
         uint8_t* wb = reinterpret_cast<uint8_t*>(sh.whist);
         __syncthreads();
 #pragma unroll 4
-        for (Idx n = tid; n < N; n += kThreads) wb[n] = (uint8_t)width(n);
+        for (Idx n = tid; n < N; n += kThreads) {
+            K2_ASSERT((size_t)n < sizeof(sh.whist));
+            wb[n] = (uint8_t)width(n);
+        }
         __syncthreads();
         const Idx CH = ((N + kWarps - 1) / kWarps + 31) / 32 * 32;
         const Idx c0 = min(N, (Idx)wid * CH), c1 = min(N, c0 + CH);
